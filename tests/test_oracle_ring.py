@@ -1,0 +1,266 @@
+"""Pins for O1 (oracle/ring.py) against things other than itself (-m "not gpu").
+
+Each pin would fail under a plausible mistake: a dropped rank, a wrong segment
+owner, a reversed fold, wrong bf16 rounding, an off-by-one in the sequences.
+"""
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+from inputs import hashgen
+from oracle import dfce, ring
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+NS = [1, 2, 3, 4, 8]
+COUNTS = [1, 7, 256, 1000, 65536]
+
+
+def _bits(a):
+    a = np.asarray(a)
+    return a.view(np.uint32) if a.dtype.itemsize == 4 else a.view(np.uint16)
+
+
+# ------------------------------------------------------------------ SPEC / paper examples
+@pytest.mark.parametrize("ex", GOLDEN["results"], ids=lambda e: e["kind"])
+def test_spec_result_examples(ex):
+    xs = [np.array(v, dtype=np.int32) for v in ex["inputs"]]
+    outs = ring.result_full(ex["kind"], ex["dtype"], xs)
+    exp = ex["expected"]
+    if len(exp) == 1:
+        exp = exp * len(xs)
+    for r, o in enumerate(outs):
+        assert o.tolist() == exp[r], ex["cite"]
+
+
+def test_spec_sequences():
+    for ex in GOLDEN["sequences"]:
+        if "per_rank" in ex:
+            for r, prims in enumerate(ex["per_rank"]):
+                got = [p for p, _ in ring.ring_sequence(ex["kind"], ex["n"], r, ex["root"], ex["inplace"])]
+                assert got == prims, ex["cite"]
+        else:
+            got = [p for p, _ in ring.ring_sequence(ex["kind"], ex["n"], ex["rank"], ex["root"], ex["inplace"])]
+            assert got == ex["prims"], ex["cite"]
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 8])
+def test_sequence_lengths_and_coverage(n):
+    """AR 2n-1 steps, AG/RS n steps, BC 1 step; every primitive has
+    a send or a recv; AR reduces every segment exactly once per rank
+    and writes every segment exactly once per rank."""
+    for r in range(n):
+        ar = ring.ring_sequence("allreduce", n, r)
+        assert len(ar) == 2 * n - 1
+        assert len(ring.ring_sequence("allgather", n, r)) == n
+        assert len(ring.ring_sequence("reducescatter", n, r)) == n
+        assert len(ring.ring_sequence("broadcast", n, r, root=n - 1)) == 1
+        for p, _ in ar:
+            rv, _, _, sd = ring.PRIMS[p]
+            assert rv or sd
+        reduced = [q for p, q in ar if ring.PRIMS[p][1]] + [q for p, q in ar if p == "Send"]
+        assert sorted(reduced) == list(range(n))
+        written = [q for p, q in ar if ring.PRIMS[p][2]]
+        assert sorted(written) == list(range(n))
+    # neighbour consistency: what rank r sends at step j, rank r+1 receives at step j+1
+    for kind in ("allreduce", "allgather", "reducescatter"):
+        for r in range(n):
+            s = ring.ring_sequence(kind, n, r)
+            d = ring.ring_sequence(kind, n, (r + 1) % n)
+            for j in range(len(s) - 1):
+                if ring.PRIMS[s[j][0]][3]:
+                    assert ring.PRIMS[d[j + 1][0]][0] and d[j + 1][1] == s[j][1]
+
+
+# ------------------------------------------------------------------ closed forms (integers)
+@pytest.mark.parametrize("n", NS)
+@pytest.mark.parametrize("count", COUNTS)
+def test_int_closed_form_allreduce(n, count):
+    """x_r[i] = (r+1)*(i mod 97 + 1) => AR = n(n+1)/2 * (i mod 97 + 1), order-free."""
+    i = np.arange(count)
+    xs = [((r + 1) * (i % 97 + 1)).astype(np.int32) for r in range(n)]
+    out = ring.allreduce(xs, "i32")
+    assert np.array_equal(out, (n * (n + 1) // 2 * (i % 97 + 1)).astype(np.int32))
+
+
+@pytest.mark.parametrize("n", NS)
+def test_int_closed_form_rs_ag_bc(n):
+    N = 37
+    xs = [np.array([1000 * q + j for j in range(n * N)], dtype=np.int32) for q in range(n)]
+    for r, o in enumerate(ring.reduce_scatter(xs, "i32")):
+        j = np.arange(N)
+        assert np.array_equal(o, sum(1000 * q + r * N + j for q in range(n)).astype(np.int32))
+    ys = [np.array([1000 * q + j for j in range(N)], dtype=np.int32) for q in range(n)]
+    ag = ring.all_gather(ys)
+    assert ag.tolist() == [1000 * q + j for q in range(n) for j in range(N)]
+    for root in range(n):
+        assert ring.broadcast(ys, root).tolist() == [1000 * root + j for j in range(N)]
+
+
+def test_int32_wraparound():
+    xs = [np.array([2**31 - 1, -2**31], dtype=np.int32), np.array([1, -1], dtype=np.int32)]
+    assert ring.allreduce(xs, "i32").tolist() == [-2**31, 2**31 - 1]
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_fp32_exact_small_integer_sums(n):
+    """x_r[i] = r*1024 + i is exact in fp32 and so is every partial sum => order-free."""
+    count = 4099
+    i = np.arange(count)
+    xs = [(r * 1024 + i).astype(np.float32) for r in range(n)]
+    out = ring.allreduce(xs, "f32")
+    assert np.array_equal(out, (sum(r * 1024 for r in range(n)) + n * i).astype(np.float32))
+
+
+# ------------------------------------------------------------------ order pins (floating point)
+def test_fp32_n2_is_order_free_sum():
+    xs = ring.inputs_full("allreduce", "f32", 2, 5000, 11, 0)
+    assert np.array_equal(_bits(ring.allreduce(xs, "f32")), _bits(xs[0] + xs[1]))
+
+
+@pytest.mark.parametrize("n", [3, 4, 8])
+def test_fp32_order_is_observable(n):
+    """Discrimination: the ring order differs from a naive rank-0-first fold on some
+    elements of random fp32 inputs, so parity tests can see a wrong order."""
+    xs = ring.inputs_full("allreduce", "f32", n, 1 << 14, 5, 3)
+    o = ring.allreduce(xs, "f32")
+    naive = xs[0].copy()
+    for q in range(1, n):
+        naive = naive + xs[q]
+    assert (_bits(o) != _bits(naive)).any()
+    # and the ring order for segment c really starts at rank c+1 and ends at c
+    L = ring.ar_segment_len(len(xs[0]), n, "f32")
+    for c in range(n):
+        seg = slice(c * L, (c + 1) * L)
+        ref = xs[(c + 1) % n][seg].copy()
+        for k in range(2, n):
+            ref = ref + xs[(c + k) % n][seg]
+        ref = ref + xs[c][seg]
+        assert np.array_equal(_bits(o[seg]), _bits(ref))
+
+
+def test_rs_equals_ar_segment_when_aligned():
+    """RS_r == AR[r*N:(r+1)*N] when N is a multiple of the vector unit (the AR owner
+    map then coincides with the RS segments) -- two different code paths."""
+    for dtype in ("f32", "bf16", "i32"):
+        n, N = 4, 1024
+        xs = ring.inputs_full("reducescatter", dtype, n, N, 9, 1)
+        ar = ring.allreduce(xs, dtype)
+        for r, o in enumerate(ring.reduce_scatter(xs, dtype)):
+            assert np.array_equal(_bits(o), _bits(ar[r * N:(r + 1) * N]))
+
+
+# ------------------------------------------------------------------ bf16 arithmetic pins
+def _bf16_correctly_rounded(a_bits, b_bits):
+    """Independent: exact rational sum, then round to 8 significant bits, ties-to-even."""
+    out = []
+    for a, b in zip(a_bits.tolist(), b_bits.tolist()):
+        fa = Fraction(float(np.array([a], dtype=np.uint16).astype(np.uint32).__lshift__(16).view(np.float32)[0]))
+        fb = Fraction(float(np.array([b], dtype=np.uint16).astype(np.uint32).__lshift__(16).view(np.float32)[0]))
+        s = fa + fb
+        if s == 0:
+            out.append(0.0)
+            continue
+        sign = -1 if s < 0 else 1
+        s = abs(s)
+        e = 0
+        while s >= 2:
+            s /= 2
+            e += 1
+        while s < 1:
+            s *= 2
+            e -= 1
+        m = s * 128                       # 8 significant bits: 1.xxxxxxx
+        fl = m.numerator // m.denominator
+        rem = m - fl
+        if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and fl % 2 == 1):
+            fl += 1
+        out.append(sign * float(Fraction(fl, 128) * Fraction(2) ** e))
+    return np.array(out, dtype=np.float32)
+
+
+def test_bf16_add_is_correctly_rounded():
+    a = hashgen.values("bf16", 1, 0, 0, np.arange(3000))
+    b = hashgen.values("bf16", 1, 0, 1, np.arange(3000))
+    got = ring.bf16_to_f32(ring.add(a, b, "bf16"))
+    assert np.array_equal(got, _bf16_correctly_rounded(a, b))
+    exact = ring.bf16_to_f32(a).astype(np.float64) + ring.bf16_to_f32(b).astype(np.float64)
+    assert (exact != got.astype(np.float64)).sum() > 100      # rounding really exercised
+
+
+@pytest.mark.parametrize("n", [2, 3, 8])
+def test_bf16_fold_matches_torch(n):
+    """Library pin: torch CPU bfloat16 addition in the same ring order."""
+    xs = ring.inputs_full("allreduce", "bf16", n, 4096, 2, 2)
+    o = ring.allreduce(xs, "bf16")
+    ts = [torch.from_numpy(x.astype(np.int16)).view(torch.bfloat16) for x in xs]
+    L = ring.ar_segment_len(4096, n, "bf16")
+    ref = torch.empty_like(ts[0])
+    for c in range(n):
+        seg = slice(c * L, (c + 1) * L)
+        acc = ts[(c + 1) % n][seg].clone()
+        for k in range(2, n):
+            acc = acc + ts[(c + k) % n][seg]
+        ref[seg] = acc + ts[c][seg]
+    assert np.array_equal(ref.view(torch.int16).numpy().view(np.uint16), o)
+
+
+def test_fp32_add_matches_torch():
+    xs = ring.inputs_full("allreduce", "f32", 3, 4096, 4, 4)
+    o = ring.allreduce(xs, "f32")
+    ts = [torch.from_numpy(x) for x in xs]
+    L = ring.ar_segment_len(4096, 3, "f32")
+    ref = torch.empty_like(ts[0])
+    for c in range(3):
+        seg = slice(c * L, (c + 1) * L)
+        ref[seg] = (ts[(c + 1) % 3][seg] + ts[(c + 2) % 3][seg]) + ts[c][seg]
+    assert np.array_equal(ref.numpy().view(np.uint32), o.view(np.uint32))
+
+
+# ------------------------------------------------------------------ segment map
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
+@pytest.mark.parametrize("n", [2, 3, 8])
+def test_segment_map_cover_and_alignment(dtype, n):
+    A = 16 // ring.ITEMSIZE[dtype]
+    for count in (1, 7, 8, 9, 63, 1000, 65537):
+        L = ring.ar_segment_len(count, n, dtype)
+        assert L % A == 0 and L * n >= count and (L - A) * n < count + n * A
+        owner = ring.ar_owner(np.arange(count), count, n, dtype)
+        assert owner.min() >= 0 and owner.max() < n
+        assert np.all(np.diff(owner) >= 0)
+
+
+# ------------------------------------------------------------------ sampled == full
+@pytest.mark.parametrize("kind", ring.KINDS)
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
+def test_expected_at_matches_full(kind, dtype):
+    n, count, seed, coll = 4, 777, 13, 5
+    xs = ring.inputs_full(kind, dtype, n, count, seed, coll)
+    full = ring.result_full(kind, dtype, xs, root=2)
+    rng = np.random.default_rng(0)
+    for r in range(n):
+        idx = rng.integers(0, len(full[r]), 200)
+        got = ring.expected_at(kind, dtype, n, count, seed, coll, idx, rank=r, root=2)
+        assert np.array_equal(_bits(got), _bits(full[r][idx]))
+
+
+# ------------------------------------------------------------------ O1 == O2 (two derivations)
+@pytest.mark.parametrize("kind", ring.KINDS)
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
+def test_o1_equals_o2_execution(kind, dtype, n):
+    """O2 executes the ring primitive sequences over connectors; its outputs must equal
+    O1's closed-form fold bit-exactly."""
+    for count, lanes, inplace in ((1, 1, False), (7, 2, False), (1000, 3, False), (2053, 2, True)):
+        m = dfce.CollMeta(0, kind, dtype, count, root=min(1, n - 1), nblocks=lanes, inplace=inplace)
+        cfg = dfce.SimConfig(lanes=lanes, K=3, slice_elems=16, slices_per_chunk=2,
+                             spin_base=8, spin_step=1, spin_min=1, spin_cap=32, seed=n)
+        sim, bufs = dfce.run_orders([m], [[0]] * n, cfg, seed=17)
+        xs = ring.inputs_full(kind, dtype, n, count, 17, 0)
+        exp = ring.result_full(kind, dtype, xs, root=m.root)
+        for r in range(n):
+            got = sim.results[(r, 0, 0)]
+            assert np.array_equal(_bits(got), _bits(exp[r])), (kind, dtype, n, count, r)
