@@ -1,0 +1,201 @@
+/*
+ * occl.h -- C-ABI of the B200-native OCCL hot path (arXiv 2303.06324).
+ *
+ * A persistent, preemptible daemon kernel (one per rank) runs ring AllReduce /
+ * AllGather / ReduceScatter / Broadcast slice by slice over peer memory
+ * (NVLink 5 / NVSwitch through CUDA IPC or peer access; plain HBM when several
+ * ranks share one device).  Ranks may submit collectives in ANY per-rank order.
+ *
+ * Paper passages each call follows (PAPER.md = /root/reference/PAPER.md, LaTeX):
+ *   - registration with unique ids, prepared before execution ... PAPER.md:373-375 (§3.1.1)
+ *   - SQE = collective id + send/recv buffer addresses ........... PAPER.md:397-398 (§3.1.2)
+ *   - Exiting SQE ................................................ PAPER.md:399     (§3.1.2)
+ *   - CQE + poller + callback map ................................ PAPER.md:401-404 (§3.1.2)
+ *   - voluntary quit / event-driven start ........................ PAPER.md:406-416 (§3.1.3)
+ *   - stickiness (order + spin-threshold policies) ............... PAPER.md:422-457 (§3.2)
+ *   - per-collective grid size, SPMC SQ, completion counters ..... PAPER.md:464-506 (§4)
+ *   - context-switch optimisations ............................... PAPER.md:509-515 (§4)
+ *
+ * Conventions (all calls):
+ *   - Every call returns occlResult_t; nothing throws or aborts across the ABI.
+ *   - Argument errors are reported synchronously.  An asynchronous device fault
+ *     makes the communicator sticky-errored; it then surfaces from
+ *     occlWait / occlTest / occlCommQuiesce as occlCudaError.
+ *   - Pointers named send/recv are DEVICE pointers on the communicator's device,
+ *     owned by the caller.  They must stay allocated, and `send` unmodified, until
+ *     occlWait / occlTest reports completion.  `send` must already hold its data
+ *     when the call is made (the invoker submits when its tensor is ready,
+ *     PAPER.md:525): synchronise the producing stream first.
+ *   - The communicator owns connectors, SQ/CQ, context buffer and daemon stream.
+ *   - collId in [0, maxColl) is GLOBALLY AGREED: every rank uses the same id for
+ *     the same logical collective with identical (kind, count, dtype, op, root).
+ *     Mismatched metadata across ranks is undefined behaviour.  An id may be
+ *     resubmitted (with new buffers) only after it completed locally
+ *     (PAPER.md:382-383); resubmitting an in-flight id returns occlDuplicateSubmit.
+ *   - In-place (NCCL conventions): send == recv (AllReduce, Broadcast);
+ *     send == recv + rank*sendcount (AllGather); recv == send + rank*recvcount
+ *     (ReduceScatter).
+ *   - count == 0 completes at submission.  One submitting host thread per
+ *     communicator at a time.  A full SQ blocks the submitter
+ *     until the daemon frees a slot.
+ */
+#ifndef OCCL_H_
+#define OCCL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct occlComm* occlComm_t;
+
+typedef enum {
+  occlSuccess = 0,
+  occlInvalidArgument = 1,   /* bad pointer/size/dtype/root/collId (SPEC.md:56 InvalidMeta)   */
+  occlInvalidUsage = 2,      /* wrong state: destroy with work in flight, not connected, ...  */
+  occlRegistryFull = 3,      /* collId >= maxColl                                              */
+  occlQueueFull = 4,         /* reserved (submission blocks instead)                           */
+  occlDuplicateSubmit = 5,   /* collId already in flight                         */
+  occlUnknownId = 6,         /* wait/test on an id never submitted               */
+  occlCudaError = 7,         /* CUDA runtime error or asynchronous device fault (sticky)       */
+  occlSystemError = 8,       /* host allocation / thread failure                               */
+  occlTimeout = 9,           /* occlWait / occlCommQuiesce timeout                              */
+  occlInProgress = 10,       /* returned by occlTest-like helpers when not complete            */
+  occlInternalError = 11     /* corrupt context or invariant violation                         */
+} occlResult_t;
+
+typedef enum { occlInt32 = 0, occlFloat32 = 1, occlBfloat16 = 2 } occlDataType_t;
+typedef enum { occlSum = 0 } occlRedOp_t;
+typedef enum { occlOrderFifo = 0, occlOrderPriority = 1 } occlOrderPolicy_t;
+
+/* Configuration.  Every rank of a communicator MUST use identical values (the
+ * per-collective block count and the slice geometry derive from them). */
+typedef struct {
+  int maxColl;            /* registry size: collId in [0, maxColl) ("up to 1,000")   */
+  int gridBlocks;         /* G: daemon grid = max blocks any collective uses        */
+  int blockThreads;       /* threads per daemon block (multiple of 32, <= 1024)                    */
+  int connSlots;          /* K: slots per connector; must exceed slicesPerChunk                    */
+  int slicesPerChunk;     /* slices each primitive moves per loop             */
+  size_t sliceBytes;      /* bytes per connector slot (multiple of 16)                             */
+  size_t minBlockBytes;   /* a collective uses ceil(segmentBytes / minBlockBytes) blocks (<= G)   */
+  int sqDepth;            /* SQ ring entries                                                       */
+  int orderPolicy;        /* occlOrderFifo | occlOrderPriority                  */
+  int priorityCadence;    /* priority policy: poll the SQ every N scheduling rounds                */
+  int stickiness;         /* 1 = paper's spin-threshold policy; 0 = constant    */
+  uint32_t spinBase;      /* initial threshold (failed connector polls) at queue position 0       */
+  uint32_t spinStep;      /* decrement per queue position                                         */
+  uint32_t spinMin;       /* floor                                                                 */
+  uint32_t spinBoost;     /* multiply on each successful primitive                                */
+  uint32_t spinCap;       /* ceiling                                                               */
+  uint32_t stallLimit;    /* preemptions without progress => "cannot progress"     */
+  int quitEnabled;        /* voluntary quit                                     */
+  uint64_t quitIdleNs;    /* quit horizon: queue empty/all stuck and no SQE for this long         */
+  uint32_t idleSleepNs;   /* back-off between empty SQ polls                                       */
+  int autoLaunch;         /* 1 = event-driven (re)start by the host supervisor */
+  int cacheWays;          /* direct-mapped shared-memory context cache ways        */
+} occlConfig_t;
+
+/* Aggregate counters (device counters summed over blocks/collectives). */
+typedef struct {
+  uint64_t launches;      /* daemon kernel launches (event-driven starts)                          */
+  uint64_t quits;         /* block-level voluntary quits                                           */
+  uint64_t exits;         /* block-level exits after the Exiting SQE                               */
+  uint64_t preemptions;   /* collective preemptions (context switches out)                         */
+  uint64_t ctxLoads;      /* context loads from the context buffer (cache misses)                  */
+  uint64_t ctxSaves;      /* lazy dynamic-context saves                                            */
+  uint64_t slices;        /* connector slices executed                                             */
+  uint64_t sqeFetched;    /* SQEs admitted into task queues                                        */
+  uint64_t cqeWritten;    /* CQEs posted                                                           */
+  float lastLaunchMs;     /* device time of the last completed daemon launch (CUDA events)         */
+} occlStats_t;
+
+typedef struct {
+  uint64_t preemptions, ctxLoads, ctxSaves, slices, completions;
+} occlCollStats_t;
+
+/* Bootstrap all-gather: gather `bytesPerRank` bytes from every rank into `out`
+ * (rank-major).  Return 0 on success. */
+typedef int (*occlAllGatherFn)(const void* in, void* out, size_t bytesPerRank, void* ctx);
+typedef void (*occlCallback_t)(int collId, void* arg);
+
+#define OCCL_HANDLE_BYTES 256
+
+const char* occlGetErrorString(occlResult_t result);
+
+/* Fill *cfg with defaults. */
+occlResult_t occlConfigDefault(occlConfig_t* cfg);
+
+/* Create rank `rank` of an `nranks` ring on CUDA device `cudaDev`: allocates the
+ * connector arena (maxColl x G x K x sliceBytes data + flags), context buffer,
+ * completion counters (device memory) and the SQ / CQ / per-block SQ cursors
+ * (pinned, mapped host memory).  cfg == NULL => defaults.  Not usable until
+ * occlCommConnect. */
+occlResult_t occlCommCreate(occlComm_t* comm, int nranks, int rank, int cudaDev,
+                            const occlConfig_t* cfg);
+
+/* Serialise this rank's handle (<= OCCL_HANDLE_BYTES bytes) into `out`; *len is
+ * in: capacity, out: bytes written.  The handle carries the arena's CUDA IPC
+ * handle, its raw device pointer, pid and device (same-process peers use the
+ * raw pointer directly). */
+occlResult_t occlCommGetHandle(occlComm_t comm, void* out, size_t* len);
+
+/* Open the ring neighbours' arenas from the rank-major array of every rank's
+ * handle (lenPerRank bytes each), enable peer access, start the supervisor. */
+occlResult_t occlCommConnect(occlComm_t comm, const void* allHandles, size_t lenPerRank);
+
+/* Create + GetHandle + ag(...) + Connect.  The paper's occlCommInit. */
+occlResult_t occlCommInit(occlComm_t* comm, int nranks, int rank, int cudaDev,
+                          occlAllGatherFn ag, void* agCtx, const occlConfig_t* cfg);
+
+/* Push the Exiting SQE, wait for the daemon to drain and exit,
+ * free everything.  occlInvalidUsage if collectives are still in flight. */
+occlResult_t occlCommDestroy(occlComm_t comm);
+
+/* Asynchronous submission (one SQE each).  Returns once the SQE is in the SQ. */
+occlResult_t occlAllReduce(const void* sendbuff, void* recvbuff, size_t count,
+                           occlDataType_t datatype, occlRedOp_t op, int collId, occlComm_t comm);
+occlResult_t occlAllGather(const void* sendbuff, void* recvbuff, size_t sendcount,
+                           occlDataType_t datatype, int collId, occlComm_t comm);
+occlResult_t occlReduceScatter(const void* sendbuff, void* recvbuff, size_t recvcount,
+                               occlDataType_t datatype, occlRedOp_t op, int collId, occlComm_t comm);
+occlResult_t occlBroadcast(const void* sendbuff, void* recvbuff, size_t count,
+                           occlDataType_t datatype, int root, int collId, occlComm_t comm);
+
+/* Block until the latest submission of collId completed locally (its CQE was
+ * posted).  timeoutNs < 0 waits forever.  occlUnknownId if never submitted. */
+occlResult_t occlWait(occlComm_t comm, int collId, int64_t timeoutNs);
+
+/* Non-blocking completion test: *done = 1 when complete. */
+occlResult_t occlTest(occlComm_t comm, int collId, int* done);
+
+/* Bind a callback fired exactly once per completion of collId by the host
+ * poller.  cb == NULL unbinds. */
+occlResult_t occlSetCallback(occlComm_t comm, int collId, occlCallback_t cb, void* arg);
+
+/* Counters (a snapshot; the daemon may be running). */
+occlResult_t occlGetStats(occlComm_t comm, occlStats_t* out);
+occlResult_t occlGetCollStats(occlComm_t comm, int collId, occlCollStats_t* out);
+
+/* --- daemon control (the paper's lifecycle made explicit) --------------------- */
+/* Push an Exiting SQE: every block drains its task queue, then exits.  A later
+ * submission restarts the daemon (event-driven start). */
+occlResult_t occlCommExit(occlComm_t comm);
+/* Launch the daemon now if it is not running (what the supervisor does on an
+ * SQE when autoLaunch = 1). */
+occlResult_t occlCommLaunch(occlComm_t comm);
+/* Enable / disable the supervisor's event-driven start. */
+occlResult_t occlCommSetAutoLaunch(occlComm_t comm, int enable);
+/* Wait until no daemon kernel of this communicator is running. */
+occlResult_t occlCommQuiesce(occlComm_t comm, int64_t timeoutNs);
+/* The CUDA stream (cudaStream_t) the daemon kernel is launched on. */
+occlResult_t occlCommGetStream(occlComm_t comm, void** stream);
+/* Number of blocks a collective of this shape uses (identical on every rank). */
+occlResult_t occlCollBlocks(occlComm_t comm, int kind, size_t count, occlDataType_t datatype,
+                            int* nblocks);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OCCL_H_ */

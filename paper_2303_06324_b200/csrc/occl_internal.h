@@ -1,0 +1,117 @@
+// occl_internal.h -- layouts shared by the host runtime (occl_host.cc) and the
+// daemon kernel (occl_daemon.cu).  Product code; shares nothing with oracle/.
+#pragma once
+#include <stdint.h>
+#include <stddef.h>
+
+namespace occl {
+
+enum Kind : uint16_t { kAllReduce = 0, kAllGather = 1, kReduceScatter = 2, kBroadcast = 3, kExit = 15 };
+enum Dtype : uint16_t { kI32 = 0, kF32 = 1, kBF16 = 2 };
+
+constexpr int kMaxRanks = 64;
+constexpr int kFlagStride = 256;        // per (coll, block): head @+0, credit @+128 (own lines)
+constexpr int kCtxBytes = 128;          // one context slot (static + dynamic), 16 B aligned
+constexpr int kMaxCacheWays = 32;
+
+// Submission queue entry: 64 B, lives in pinned+mapped host memory.
+// `seq` is written LAST by the host (release); the daemon accepts the slot iff
+// seq == its cursor + 1.
+struct alignas(64) Sqe {
+  uint64_t seq;        // 1-based index of this SQE in the SQ stream
+  uint64_t subSeq;     // per-collective submission number (what the CQ reports)
+  uint64_t count;      // AR/BC: elements; AG: sendcount; RS: recvcount
+  uint64_t sendbuff;
+  uint64_t recvbuff;
+  uint32_t collId;
+  uint16_t kind;
+  uint16_t dtype;
+  uint16_t op;
+  uint16_t nblocks;    // the collective's grid size
+  int32_t root;
+  uint32_t pad[2];
+};
+static_assert(sizeof(Sqe) == 64, "Sqe must be 64 B");
+
+// Static context: constant for one submission.  48 B.
+struct alignas(16) StaticCtx {
+  uint64_t sendbuff;
+  uint64_t recvbuff;
+  uint64_t subSeq;
+  uint64_t segLen;     // elements per segment (AR: L; RS/AG: count; BC: count)
+  uint64_t part;       // elements of each segment handled by one block (Pb)
+  uint64_t count;
+};
+// Dynamic context: chunk (loop) id, primitive (step) id,
+// slice id, plus the connector sequence numbers (heads/credits are monotonic per
+// (collective, block) across submissions).  32 B.
+struct alignas(16) DynCtx {
+  uint32_t loop;
+  uint16_t step;
+  uint16_t slc;
+  uint32_t nloops;
+  uint16_t kind;
+  uint8_t dtype;
+  uint8_t progressed;
+  uint64_t nsent;      // slices pushed into the downstream connector so far
+  uint64_t nrecv;      // slices consumed from the upstream connector so far
+};
+struct alignas(16) CtxSlot {
+  StaticCtx s;         // 48
+  DynCtx d;            // 32
+  int32_t root;        // meta that also belongs to the static part
+  uint16_t nblocks;
+  uint16_t nsteps;
+  uint32_t pad[8];
+};
+static_assert(sizeof(CtxSlot) == kCtxBytes, "CtxSlot must be 128 B");
+
+// Per-block state that survives a voluntary quit.
+struct alignas(16) BlockState {
+  uint64_t sqCursor;   // SQEs consumed by this block
+  uint32_t qlen;       // task queue length at quit
+  uint32_t pos;
+  uint32_t exiting;    // Exiting SQE consumed, not yet drained
+  uint32_t pad;
+};
+
+struct alignas(16) CollStat {   // per (collective, block), device memory
+  unsigned long long preemptions, ctxLoads, ctxSaves, slices, completions, pad[3];
+};
+struct alignas(16) BlockStat {  // per block
+  unsigned long long quits, exits, fetched, cqes, launches, idlePolls, pad[2];
+};
+
+struct DaemonParams {
+  const Sqe* sq;                    // mapped host SQ
+  volatile uint64_t* sqCursorHost;  // mapped host [G]
+  volatile uint64_t* cqDone;        // mapped host [maxColl]: last completed subSeq
+  BlockState* blk;                  // [G]
+  uint32_t* tqSave;                 // [G][maxColl] packed (id | stall << 16)
+  CtxSlot* ctx;                     // [maxColl][G]
+  uint32_t* complCnt;               // [maxColl]
+  CollStat* collStats;              // [maxColl][G]
+  BlockStat* blkStats;              // [G]
+  char* dataLocal;                  // this rank's connector data [maxColl][G][K][sliceBytes]
+  char* dataNext;                   // downstream rank's connector data
+  char* flagsLocal;                 // [maxColl][G] x kFlagStride
+  char* flagsNext;
+  char* flagsPrev;
+  uint64_t sliceBytes;
+  uint32_t sqDepth;
+  int nranks, rank, G, maxColl, K, slicesPerChunk;
+  int orderPolicy, priorityCadence, stickiness;
+  uint32_t spinBase, spinStep, spinMin, spinBoost, spinCap, stallLimit;
+  int quitEnabled;
+  uint64_t quitIdleNs;
+  uint32_t idleSleepNs;
+  int cacheWays;
+  int sysScope;                     // 1: peers in other processes/devices -> .sys fences
+};
+
+}  // namespace occl
+
+// Launch entry implemented in occl_daemon.cu (internal, not part of the C-ABI).
+extern "C" int occl_internal_launch_daemon(const occl::DaemonParams* p, const occl::DaemonParams* pDev,
+                                           int blockThreads, void* stream);
+extern "C" size_t occl_internal_daemon_smem(int maxColl, int cacheWays);

@@ -1,0 +1,106 @@
+"""Helpers for the -m gpu parity tests: device buffers from the seeded generator,
+expected values from the CPU oracle (O1), element-by-element comparison."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from inputs import hashgen
+from oracle import ring
+from paper_2303_06324_b200 import occl
+
+TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32}
+WAIT_S = 60.0
+
+
+def bits(a):
+    a = np.asarray(a)
+    return a.view(np.uint32) if a.dtype.itemsize == 4 else a.view(np.uint16)
+
+
+def to_np_bits(t: torch.Tensor) -> np.ndarray:
+    t = t.detach().cpu()
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).numpy().view(np.uint16)
+    if t.dtype == torch.float32:
+        return t.numpy().view(np.uint32)
+    return t.numpy().view(np.uint32)
+
+
+def in_len(kind, n, count):
+    return count * n if kind == "reducescatter" else count
+
+
+def out_len(kind, n, count):
+    return count * n if kind == "allgather" else count
+
+
+def make_bufs(kind, dtype, n, count, seed, coll, device=0, inplace=False):
+    """Per-rank (send, recv) device tensors; send filled by the GPU generator."""
+    sends, recvs = [], []
+    for r in range(n):
+        if inplace:
+            if kind in ("allreduce", "broadcast"):
+                buf = torch.empty(count, dtype=TORCH_DT[dtype], device=device)
+                occl.test_fill(buf, dtype, seed, coll, r)
+                sends.append(buf)
+                recvs.append(buf)
+            elif kind == "allgather":
+                buf = torch.full((count * n,), 0, dtype=TORCH_DT[dtype], device=device)
+                s = buf[r * count:(r + 1) * count]
+                occl.test_fill(s, dtype, seed, coll, r)
+                sends.append(s)
+                recvs.append(buf)
+            else:  # reducescatter: recv == send + rank*recvcount
+                buf = torch.empty(count * n, dtype=TORCH_DT[dtype], device=device)
+                occl.test_fill(buf, dtype, seed, coll, r)
+                sends.append(buf)
+                recvs.append(buf[r * count:(r + 1) * count])
+        else:
+            s = torch.empty(in_len(kind, n, count), dtype=TORCH_DT[dtype], device=device)
+            occl.test_fill(s, dtype, seed, coll, r)
+            rv = torch.full((out_len(kind, n, count),), -7, dtype=TORCH_DT[dtype], device=device) \
+                if dtype != "bf16" else torch.zeros(out_len(kind, n, count), dtype=torch.bfloat16, device=device)
+            sends.append(s)
+            recvs.append(rv)
+    torch.cuda.synchronize()
+    return sends, recvs
+
+
+def expected_full(kind, dtype, n, count, seed, coll, root=0):
+    xs = ring.inputs_full(kind, dtype, n, count, seed, coll)
+    return [bits(o) for o in ring.result_full(kind, dtype, xs, root=root)]
+
+
+def check_full(kind, dtype, n, count, seed, coll, recvs, root=0):
+    exp = expected_full(kind, dtype, n, count, seed, coll, root)
+    for r in range(n):
+        got = to_np_bits(recvs[r])
+        if not np.array_equal(got, exp[r]):
+            bad = np.nonzero(got != exp[r])[0]
+            raise AssertionError(f"{kind} {dtype} n={n} count={count} rank {r}: {len(bad)} mismatches, "
+                                 f"first at {bad[:8].tolist()} got {got[bad[:4]].tolist()} exp {exp[r][bad[:4]].tolist()}")
+
+
+def check_sampled(kind, dtype, n, count, seed, coll, recvs, root=0, nsamples=4096, boundaries=()):
+    """Sampled comparison at full sizes: random indices + segment/block boundaries."""
+    rng = np.random.default_rng(seed ^ coll)
+    for r in range(n):
+        L = out_len(kind, n, count)
+        idx = np.concatenate([rng.integers(0, L, nsamples), np.array([0, L - 1], dtype=np.int64),
+                              np.array([b for b in boundaries if 0 <= b < L], dtype=np.int64)])
+        idx = np.unique(idx)
+        got = to_np_bits(recvs[r][torch.from_numpy(idx).to(recvs[r].device)])
+        exp = bits(ring.expected_at(kind, dtype, n, count, seed, coll, idx, rank=r, root=root))
+        if not np.array_equal(got, exp):
+            bad = np.nonzero(got != exp)[0]
+            raise AssertionError(f"{kind} {dtype} n={n} count={count} rank {r}: {len(bad)} sampled mismatches "
+                                 f"at {idx[bad[:8]].tolist()}")
+
+
+def run_collective(comms, kind, sends, recvs, coll, count, dtype, root=0, order=None):
+    order = order if order is not None else range(len(comms))
+    for r in order:
+        comms[r].submit(kind, sends[r], recvs[r], coll, count, dtype, root)
+    for c in comms:
+        c.wait(coll, WAIT_S)
