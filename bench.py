@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark: all-reduce bus bandwidth of the OCCL daemon path on B200.
+
+Workload (BASELINE.json configs[1], the C2 sweep's headline point): a ring of
+R = 8 ranks (--ranks) all-reducing S = 256 MiB (--size-mib) of fp32 per rank,
+sum, out of place.  The 8 ranks are spread over the N GPUs of the job: each GPU
+hosts R/N ranks (virtual ranks sharing HBM, served by ONE fused daemon launch);
+at N = 8 every rank is its own B200 and the ring runs over NVLink (IPC).  Total
+work is fixed as N grows ("scaling": "strong").
+
+A step = one all-reduce on every rank.  K steps are submitted to the SQ (one
+SQE per rank per step, distinct collective ids) with an Exiting SQE, then the
+daemon is launched once; the timed region is bracketed by CUDA events on the
+daemon's stream (plus barrier + synchronize on both sides).  Inputs (8 x 256
+MiB = 2 GiB) are larger than L2.
+
+value = nccl-tests bus bandwidth busbw = S * 2(R-1)/R / t_step   (GB/s, 1e9)
+
+--impl reference times the CPU oracle (oracle/ring.py, the plain numpy ring
+fold) on a bounded sample of the same workload on this box's host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+MiB = 1 << 20
+METRIC = "allreduce bus GB/s (8-rank ring, fp32 sum)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="occl", choices=["occl", "reference"])
+    ap.add_argument("--size-mib", type=float, default=256.0)
+    ap.add_argument("--ranks", type=int, default=8)
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "i32"])
+    ap.add_argument("--grid-blocks", type=int, default=16)
+    ap.add_argument("--slice-kib", type=int, default=64)
+    ap.add_argument("--conn-slots", type=int, default=4)
+    ap.add_argument("--slices-per-chunk", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--check", action="store_true", help="sampled oracle check of the timed output")
+    return ap.parse_args()
+
+
+def busbw(size_bytes, nranks, t_s):
+    return size_bytes * 2 * (nranks - 1) / nranks / t_s / 1e9
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ============================================================================ clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML during the timed region."""
+
+    def __init__(self, dev=0, period=0.005):
+        self.dev, self.period, self.samples, self.reasons = dev, period, [], set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(dev)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception:
+            self.N = None
+
+    def _run(self):
+        N = self.N
+        names = {}
+        for nm in ("HwSlowdown", "HwThermalSlowdown", "SwThermalSlowdown", "SwPowerCap", "HwPowerBrakeSlowdown"):
+            v = getattr(N, "nvmlClocksEventReason" + nm, None) or getattr(N, "nvmlClocksThrottleReason" + nm, None)
+            if v is not None:
+                names[v] = nm
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                mask = N.nvmlDeviceGetCurrentClocksEventReasons(self.h) if hasattr(
+                    N, "nvmlDeviceGetCurrentClocksEventReasons") else N.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, nm in names.items():
+                    if mask & bit:
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.N:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.N:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ============================================================================ reference arm
+def cpu_oracle_busbw(nranks, dtype, size_bytes, budget_s=10.0, min_reps=1, max_reps=1000):
+    """Time the CPU oracle (O1 ring fold) on a bounded sample; returns (busbw, sample, cores, secs)."""
+    from inputs import hashgen
+    from oracle import ring
+    item = hashgen.ITEMSIZE[dtype]
+    sample_bytes = min(size_bytes, 32 * MiB)
+    count = int(sample_bytes // item)
+    xs = [hashgen.buffer(dtype, 1, 0, r, count) for r in range(nranks)]
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < min_reps or (time.perf_counter() - t_all < budget_s and len(times) < max_reps):
+        t0 = time.perf_counter()
+        ring.allreduce(xs, dtype)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    sample = (f"{nranks} ranks x {sample_bytes / MiB:g} MiB {dtype} per rank (of {size_bytes / MiB:g} MiB), "
+              f"oracle/ring.py allreduce (numpy ring fold), median of {len(times)} reps")
+    return busbw(sample_bytes, nranks, t), sample, 1, sum(times)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    size = int(args.size_mib * MiB)
+    from inputs import hashgen
+    from oracle import ring
+    item = hashgen.ITEMSIZE[args.dtype]
+    sample_bytes = min(size, 32 * MiB)
+    count = int(sample_bytes // item)
+    xs = [hashgen.buffer(args.dtype, 1, 0, r, count) for r in range(args.ranks)]
+    for _ in range(args.warmup):
+        ring.allreduce(xs, args.dtype)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ring.allreduce(xs, args.dtype)
+    t = (time.perf_counter() - t0) / max(1, args.steps)
+    v = busbw(sample_bytes, args.ranks, t)
+    sample = (f"{args.ranks} ranks x {sample_bytes / MiB:g} MiB {args.dtype} per rank per step (bounded sample of "
+              f"the {args.size_mib:g} MiB workload), oracle/ring.py numpy ring fold")
+    unit = "GB/s"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (counter-based hash generator)",
+        "config": {"workload": f"C2 allreduce, {args.ranks}-rank ring, {args.size_mib:g} MiB/rank {args.dtype} sum",
+                   "ranks": args.ranks, "size_bytes_per_rank": size},
+        "cpu_baseline": {"value": v, "unit": unit, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+    return 0
+
+
+# ============================================================================ OCCL arm
+def setup_dist(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    return world, rank, local, dist
+
+
+def make_ring(args, world, prank, dev, dist):
+    """R ranks over `world` processes, V = R/world consecutive ranks per process;
+    handles exchanged over torch.distributed; local ranks fused into one daemon."""
+    from paper_2303_06324_b200 import occl
+    R = args.ranks
+    if R % world:
+        raise SystemExit("--ranks must be a multiple of the GPU count")
+    V = R // world
+    cfg = occl.occlConfigDefault(gridBlocks=args.grid_blocks, sliceBytes=args.slice_kib * 1024,
+                                 connSlots=args.conn_slots, slicesPerChunk=args.slices_per_chunk,
+                                 maxColl=128, autoLaunch=0)
+    hs = [occl.occlCommCreate(R, prank * V + i, dev, cfg) for i in range(V)]
+    mine = [occl.occlCommGetHandle(h) for h in hs]
+    if dist is not None:
+        allh = [None] * world
+        dist.all_gather_object(allh, mine)
+        handles = [h for part in allh for h in part]
+    else:
+        handles = mine
+    for h in hs:
+        occl.occlCommConnect(h, handles)
+    comms = [occl.Comm(h, R, prank * V + i, dev, cfg) for i, h in enumerate(hs)]
+    if V > 1:
+        occl.occlCommFuse(comms)
+    return comms, V
+
+
+def run_occl(args):
+    import torch
+    from paper_2303_06324_b200 import occl
+
+    world, prank, local, dist = setup_dist(args)
+    dev = local
+    torch.cuda.set_device(dev)
+    R = args.ranks
+    size = int(args.size_mib * MiB)
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32}[args.dtype]
+    item = torch.tensor([], dtype=tdt).element_size()
+    count = size // item
+    comms, V = make_ring(args, world, prank, dev, dist)
+    sends = [torch.empty(count, dtype=tdt, device=dev) for _ in range(V)]
+    recvs = [torch.empty(count, dtype=tdt, device=dev) for _ in range(V)]
+    for i, c in enumerate(comms):
+        occl.test_fill(sends[i], args.dtype, 1, 0, c.rank)
+    torch.cuda.synchronize()
+    stream = torch.cuda.ExternalStream(comms[0].stream(), device=dev)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def run_steps(nsteps, first_id=0):
+        """nsteps all-reduces per rank in ONE daemon launch; returns device ms."""
+        ids = [(first_id + k) % 120 for k in range(nsteps)]
+        for i, c in enumerate(comms):
+            for cid in ids:
+                c.all_reduce(sends[i], recvs[i], cid)
+            c.exit()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        comms[0].launch()                      # one fused launch serves all V local ranks
+        e1.record(stream)
+        for c in comms:
+            for cid in set(ids):
+                c.wait(cid, 600)
+        comms[0].quiesce(600)
+        e1.synchronize()
+        return e0.elapsed_time(e1)
+
+    steps_per_launch = 100
+    # warm-up (untimed)
+    w = args.warmup
+    while w > 0:
+        run_steps(min(w, steps_per_launch))
+        w -= steps_per_launch
+    barrier()
+    torch.cuda.synchronize()
+    before = [c.stats() for c in comms]
+    ms_total, launches, left = 0.0, 0, args.steps
+    with ClockSampler(dev) as clk:
+        while left > 0:
+            k = min(left, steps_per_launch)
+            ms_total += run_steps(k)
+            launches += 1
+            left -= k
+    torch.cuda.synchronize()
+    barrier()
+    after = [c.stats() for c in comms]
+    if dist is not None:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = busbw(size, R, ms_step / 1e3)
+
+    check = None
+    if args.check:
+        import numpy as np
+        from oracle import ring
+        rng = np.random.default_rng(0)
+        idx = np.unique(np.concatenate([rng.integers(0, count, 20000), [0, count - 1]]))
+        ok = True
+        for i, c in enumerate(comms):
+            got = recvs[i][torch.from_numpy(idx).to(dev)].cpu()
+            got = got.view(torch.int16).numpy().view(np.uint16) if args.dtype == "bf16" else got.numpy().view(np.uint32)
+            exp = ring.expected_at("allreduce", args.dtype, R, count, 1, 0, idx)
+            exp = exp.view(np.uint16) if args.dtype == "bf16" else exp.view(np.uint32)
+            ok &= bool(np.array_equal(got, exp))
+        check = {"sampled_elements_per_rank": int(len(idx)), "bit_exact": ok}
+
+    # ------------------------------------------------------------------ e2e (public API, host buffers)
+    e2e = None
+    if not args.no_e2e:
+        host_in = [torch.empty(count, dtype=tdt, pin_memory=True) for _ in range(V)]
+        for i in range(V):
+            host_in[i].copy_(sends[i].cpu())
+        host_out = torch.empty(count, dtype=tdt, pin_memory=True)
+        for c in comms:
+            c.set_auto_launch(True)
+        cs = torch.cuda.Stream(device=dev)
+        e2e_steps = max(3, min(args.steps, 10))
+
+        def e2e_step(k):
+            with torch.cuda.stream(cs):
+                for i in range(V):
+                    sends[i].copy_(host_in[i], non_blocking=True)
+            cs.synchronize()
+            cid = 120 + (k % 4)
+            for i, c in enumerate(comms):
+                c.all_reduce(sends[i], recvs[i], cid)
+            for c in comms:
+                c.wait(cid, 600)
+            if prank == 0:
+                with torch.cuda.stream(cs):
+                    host_out.copy_(recvs[0], non_blocking=True)
+                cs.synchronize()
+
+        e2e_step(0)
+        barrier()
+        t0 = time.perf_counter()
+        for k in range(e2e_steps):
+            e2e_step(k + 1)
+        barrier()
+        te = (time.perf_counter() - t0) / e2e_steps
+        if dist is not None:
+            t = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        e2e = {"value": busbw(size, R, te), "unit": "GB/s", "h2d_bytes_per_step": V * size,
+               "d2h_bytes_per_step": size if prank == 0 else 0, "ms_per_step": te * 1e3, "steps": e2e_steps,
+               "path": "pinned host -> device copies + occlAllReduce (event-driven daemon) + occlWait + D2H"}
+
+    # ------------------------------------------------------------------ roofline
+    peaks = measured_peaks()
+    slices = sum(a["slices"] - b["slices"] for a, b in zip(after, before))
+    avg_launch_ms = ms_total / max(1, launches)
+    if world == 1:
+        # One fused daemon launch serves all R ranks of this GPU; the unavoidable
+        # DRAM traffic of an on-device all-reduce is reading every rank's input and
+        # writing every rank's output: 2 * S per rank per step.
+        alg_bytes = 2 * size * V * (args.steps / launches)
+        achieved = alg_bytes / (avg_launch_ms / 1e3) / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+        if os.path.exists(tf):
+            try:
+                d = json.load(open(tf))
+                key = f"{R}x{args.size_mib:g}MiB-{args.dtype}-G{args.grid_blocks}-s{args.slice_kib}k"
+                if key in d:
+                    traffic = d[key]["dram_bytes_per_step"] * (args.steps / launches)
+            except Exception:
+                traffic = None
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else
+                    "fallback 6650 GB/s (B200_PROFILING.md)",
+                    "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_launch_ms}
+    else:
+        alg_bytes = size * 2 * (R - 1) / R * V * (args.steps / launches)     # NVLink egress per GPU
+        achieved = alg_bytes / (avg_launch_ms / 1e3) / 1e9
+        roofline = {"bound": "nvlink", "achieved": achieved, "peak": 770.0, "unit": "GB/s", "frac": achieved / 770.0,
+                    "traffic": None, "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)",
+                    "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_launch_ms}
+
+    cpu = None
+    if world == 1 and prank == 0 and not args.no_cpu:
+        v, sample, cores, secs = cpu_oracle_busbw(R, args.dtype, size)
+        cpu = {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample,
+               "cpu_seconds": secs, "host_cpus": os.cpu_count()}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic (counter-based hash generator, inputs resident in HBM)",
+        "config": {"workload": f"C2 allreduce, {R}-rank ring, {args.size_mib:g} MiB/rank {args.dtype} sum, "
+                               f"{V} rank(s) per GPU" + (" (virtual ranks, one fused daemon)" if V > 1 else ""),
+                   "ranks": R, "ranks_per_gpu": V, "size_bytes_per_rank": size, "grid_blocks": args.grid_blocks,
+                   "slice_bytes": args.slice_kib * 1024, "conn_slots": args.conn_slots,
+                   "slices_per_chunk": args.slices_per_chunk, "l2": "inputs larger than L2 (R x S >> 126 MB)",
+                   "algbw_GBps": size / (ms_step / 1e3) / 1e9},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "daemon": {"slices": slices, "preemptions": sum(a["preemptions"] - b["preemptions"] for a, b in zip(after, before)),
+                   "cqe": sum(a["cqeWritten"] - b["cqeWritten"] for a, b in zip(after, before))},
+    }
+    if check is not None:
+        line["check"] = check
+    if prank == 0:
+        print(json.dumps(line))
+    occl.destroy_group(comms)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_occl(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -145,6 +145,14 @@ occlResult_t occlCommGetHandle(occlComm_t comm, void* out, size_t* len);
  * handle (lenPerRank bytes each), enable peer access, start the supervisor. */
 occlResult_t occlCommConnect(occlComm_t comm, const void* allHandles, size_t lenPerRank);
 
+/* Serve `n` connected communicators of THIS process that live on the same device
+ * with ONE daemon kernel launch: blocks [i*G, (i+1)*G) run comms[i]'s daemon,
+ * each with its own SQ, CQ, contexts and connectors.  Used for several (virtual)
+ * ranks sharing one B200: their daemons are co-resident by construction and are
+ * started, stopped and timed together.  All must share gridBlocks, maxColl,
+ * cacheWays and blockThreads, be idle and have nothing in flight. */
+occlResult_t occlCommFuse(occlComm_t* comms, int n);
+
 /* Create + GetHandle + ag(...) + Connect.  The paper's occlCommInit. */
 occlResult_t occlCommInit(occlComm_t* comm, int nranks, int rank, int cudaDev,
                           occlAllGatherFn ag, void* agCtx, const occlConfig_t* cfg);

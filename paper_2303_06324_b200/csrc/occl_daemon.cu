@@ -157,13 +157,12 @@ template <> __device__ __forceinline__ uint16_t sadd<kBF16>(uint16_t a, uint16_t
 // loads in flight per thread, then the stores.  The action
 // bits are warp-uniform runtime flags; only the element type is a template.
 template <int DT>
-__device__ __forceinline__ void move_slice(const SliceDesc& d) {
+__device__ __forceinline__ void move_slice(const SliceDesc& d, const int tid, const int nt) {
   typedef typename Elem<DT>::T T;
   constexpr int A = 16 / sizeof(T);
   constexpr int U = 4;
   const int prim = d.prim;
   const bool recv = prim & A_RECV, reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
-  const int tid = threadIdx.x, nt = blockDim.x;
   const int n = (int)d.nelem;                     // <= sliceBytes / sizeof(T)
   if (n <= 0) return;
   const bool aligned = ((((uintptr_t)d.src) | ((uintptr_t)d.dst)) & 15) == 0;
@@ -206,10 +205,10 @@ __device__ __forceinline__ void move_slice(const SliceDesc& d) {
   }
 }
 
-__device__ __forceinline__ void move_slice_any(const SliceDesc& d) {
-  if (d.dtype == kBF16) move_slice<kBF16>(d);
-  else if (d.dtype == kF32) move_slice<kF32>(d);
-  else move_slice<kI32>(d);
+__device__ __forceinline__ void move_slice_any(const SliceDesc& d, const int tid, const int nt) {
+  if (d.dtype == kBF16) move_slice<kBF16>(d, tid, nt);
+  else if (d.dtype == kF32) move_slice<kF32>(d, tid, nt);
+  else move_slice<kI32>(d, tid, nt);
 }
 
 // ------------------------------------------------------------------ ring sequences
@@ -267,19 +266,51 @@ __device__ __forceinline__ void seg_geom(int kind, int n, int r, uint64_t count,
   }
 }
 
+// ------------------------------------------------------------------ mbarriers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+               " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile("{\n .reg .pred p;\n LAB_WAIT_%=:\n"
+               " mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+               " @!p bra LAB_WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
 // ------------------------------------------------------------------ shared control
 enum : int { CMD_NONE = 0, CMD_RUN = 1, CMD_EXIT = 2 };
 enum : int { RUN_PREEMPT = 0, RUN_GO = 1, RUN_DONE = 2 };
+constexpr int P_EXIT = 0x100;          // descriptor telling the data warps to leave
+constexpr int kDepth = 2;              // slices in flight between control and data warps
 
-// Scheduler state of one block.  Lives in shared memory and is touched only by
-// thread 0, so it costs the data-moving threads no registers.
+// Scheduler state of one block; touched only by the control thread.
 struct Sched {
   uint64_t cursor, lastFetch, iter;
   uint64_t T, headSeen, creditSeen;
   uint32_t qlen, pos, exiting;
   int lastRun, curId;
-  int cmd, way, needLoad, go;
-  SliceDesc desc;
+  int way;
+  DynCtx di;                            // issue cursor (runs ahead of the committed cx.d)
+};
+
+// Control -> data warp pipeline: slice descriptors in a ring of kDepth buffers;
+// full[i] completes when the control thread published ring[i], empty[i] when
+// every data warp finished moving it.
+struct Pipe {
+  SliceDesc ring[kDepth];
+  uint64_t full[kDepth];
+  uint64_t empty[kDepth];
 };
 
 struct Smem {
@@ -288,17 +319,17 @@ struct Smem {
   uint32_t* tq;        // [maxColl] task queue: id | stall << 16
 };
 
-__device__ __forceinline__ void save_dyn(CtxSlot* g, const CtxSlot& cx) {
+__device__ __forceinline__ void save_dyn(CtxSlot* g, const DynCtx& d) {
   uint4* gd = reinterpret_cast<uint4*>(&g->d);
-  const uint4* sd = reinterpret_cast<const uint4*>(&cx.d);
+  const uint4* sd = reinterpret_cast<const uint4*>(&d);
   st_cg_v4(gd, sd[0]);
   st_cg_v4(gd + 1, sd[1]);
 }
 
 // Admit an SQE into this block's task queue: write the static context and reset
 // the dynamic cursor (keeping the connector sequence numbers).
-__device__ __noinline__ void admit(const DaemonParams& p, Sched& sh, const Smem& m, const Sqe& e) {
-  const int b = blockIdx.x, G = p.G, n = p.nranks, W = p.cacheWays;
+__device__ __noinline__ void admit(const DaemonParams& p, int b, Sched& sh, const Smem& m, const Sqe& e) {
+  const int G = p.G, n = p.nranks, W = p.cacheWays;
   const int c = (int)e.collId;
   CtxSlot* g = &p.ctx[(size_t)c * G + b];
   const int isz = elem_size(e.dtype);
@@ -341,10 +372,10 @@ __device__ __noinline__ void admit(const DaemonParams& p, Sched& sh, const Smem&
   p.blkStats[b].fetched++;
 }
 
-// One scheduling round (thread 0): bookkeeping of the previous run, SQ fetch,
-// entry selection, voluntary quit.  Sets sh.cmd.
-__device__ __noinline__ void schedule(const DaemonParams& p, Sched& sh, const Smem& m) {
-  const int b = blockIdx.x, G = p.G, W = p.cacheWays;
+// One scheduling round: bookkeeping of the previous run, SQ fetch, entry
+// selection, voluntary quit.  Returns CMD_*.
+__device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, const Smem& m) {
+  const int G = p.G, W = p.cacheWays;
   int cmd = CMD_NONE;
   if (sh.lastRun >= 0) {
     CtxSlot& cx = m.cache[sh.way];
@@ -357,7 +388,7 @@ __device__ __noinline__ void schedule(const DaemonParams& p, Sched& sh, const Sm
       // release store suffices (R9).
       cs.completions++;
       cx.d.progressed = 0;
-      save_dyn(g, cx);
+      save_dyn(g, cx.d);
       fence_acq_rel(1);
       const uint32_t old = atom_add_acq_rel(&p.complCnt[id], 1u);
       if (old + 1 == cx.nblocks) {
@@ -373,7 +404,7 @@ __device__ __noinline__ void schedule(const DaemonParams& p, Sched& sh, const Sm
       // preempted: lazy save of a dynamic context that progressed
       if (cx.d.progressed) {
         cx.d.progressed = 0;
-        save_dyn(g, cx);
+        save_dyn(g, cx.d);
         cs.ctxSaves++;
       }
       cs.preemptions++;
@@ -392,7 +423,6 @@ __device__ __noinline__ void schedule(const DaemonParams& p, Sched& sh, const Sm
   // -- fetch an SQE, gated by the order policy
   const bool canFetch = !sh.exiting && qlen < (uint32_t)p.maxColl &&
                         (qlen == 0 || (p.orderPolicy == 0 ? allStalled : (sh.iter % (uint64_t)p.priorityCadence) == 0));
-  bool fetched = false;
   if (canFetch) {
     const Sqe* slot = p.sq + (sh.cursor % p.sqDepth);
     const uint64_t seq = ld_acquire_sys(&slot->seq);
@@ -407,65 +437,82 @@ __device__ __noinline__ void schedule(const DaemonParams& p, Sched& sh, const Sm
       fence_sys();                                   // SQE reads complete before the slot is freed
       st_volatile_u64(&p.sqCursorHost[b], sh.cursor);
       sh.lastFetch = now;
-      fetched = true;
       if (e.kind == kExit) sh.exiting = 1;          // Exiting SQE
-      else if (b < (int)e.nblocks) admit(p, sh, m, e);   // blockIdx < grid size (reading Q11)
+      else if (b < (int)e.nblocks) admit(p, b, sh, m, e);   // blockIdx < grid size (reading Q11)
+      return CMD_NONE;
     }
   }
-  if (!fetched) {
-    const bool stuck = qlen == 0 || allStalled;
-    if (qlen == 0 && sh.exiting) {
-      sh.exiting = 0;
-      p.blkStats[b].exits++;
-      cmd = CMD_EXIT;
-    } else if (stuck && p.quitEnabled && now - sh.lastFetch > p.quitIdleNs) {
-      p.blkStats[b].quits++;                         // voluntary quit
-      cmd = CMD_EXIT;
-    } else if (qlen > 0) {
-      const int c = (int)(m.tq[sh.pos] & 0xffffu);
-      const int way = c % W;
-      sh.way = way;
-      sh.needLoad = m.cacheTag[way] != c;
-      if (sh.needLoad) {
-        m.cacheTag[way] = c;
-        p.collStats[(size_t)c * G + b].ctxLoads++;
-      }
-      sh.curId = c;
-      // initial spin threshold from the queue position
-      if (p.stickiness) {
-        const uint64_t dec = (uint64_t)sh.pos * p.spinStep;
-        uint64_t T = dec >= p.spinBase ? p.spinMin : p.spinBase - dec;
-        sh.T = T < p.spinMin ? p.spinMin : T;
-      } else {
-        sh.T = p.spinBase;
-      }
-      sh.headSeen = 0;
-      sh.creditSeen = 0;
-      cmd = CMD_RUN;
+  const bool stuck = qlen == 0 || allStalled;
+  if (qlen == 0 && sh.exiting) {
+    sh.exiting = 0;
+    p.blkStats[b].exits++;
+    cmd = CMD_EXIT;
+  } else if (stuck && p.quitEnabled && now - sh.lastFetch > p.quitIdleNs) {
+    p.blkStats[b].quits++;                           // voluntary quit
+    cmd = CMD_EXIT;
+  } else if (qlen > 0) {
+    const int c = (int)(m.tq[sh.pos] & 0xffffu);
+    const int way = c % W;
+    sh.way = way;
+    if (m.cacheTag[way] != c) {
+      // context load into the shared-memory cache: 8 independent 16-B loads in
+      // flight
+      m.cacheTag[way] = c;
+      const uint4* gsrc = reinterpret_cast<const uint4*>(&p.ctx[(size_t)c * G + b]);
+      uint4 v[kCtxBytes / 16];
+#pragma unroll
+      for (int i = 0; i < kCtxBytes / 16; ++i) v[i] = ld_cg(gsrc + i);
+      uint4* dst = reinterpret_cast<uint4*>(&m.cache[way]);
+#pragma unroll
+      for (int i = 0; i < kCtxBytes / 16; ++i) dst[i] = v[i];
+      p.collStats[(size_t)c * G + b].ctxLoads++;
+    }
+    sh.curId = c;
+    // initial spin threshold from the queue position
+    if (p.stickiness) {
+      const uint64_t dec = (uint64_t)sh.pos * p.spinStep;
+      uint64_t T = dec >= p.spinBase ? p.spinMin : p.spinBase - dec;
+      sh.T = T < p.spinMin ? p.spinMin : T;
     } else {
-      p.blkStats[b].idlePolls++;
-      if (p.idleSleepNs) __nanosleep(p.idleSleepNs);
+      sh.T = p.spinBase;
     }
-    if (cmd == CMD_EXIT) {                           // persist what survives the quit
-      BlockState bs;
-      bs.sqCursor = sh.cursor; bs.qlen = sh.qlen; bs.pos = sh.pos; bs.exiting = sh.exiting; bs.pad = 0;
-      p.blk[b] = bs;
-      for (uint32_t i = 0; i < sh.qlen; ++i) p.tqSave[(size_t)b * p.maxColl + i] = m.tq[i];
-    }
+    sh.headSeen = 0;
+    sh.creditSeen = 0;
+    sh.di = m.cache[way].d;
+    cmd = CMD_RUN;
+  } else {
+    p.blkStats[b].idlePolls++;
+    if (p.idleSleepNs) __nanosleep(p.idleSleepNs);
   }
-  sh.cmd = cmd;
+  if (cmd == CMD_EXIT) {                             // persist what survives the quit
+    BlockState bs;
+    bs.sqCursor = sh.cursor; bs.qlen = sh.qlen; bs.pos = sh.pos; bs.exiting = sh.exiting; bs.pad = 0;
+    p.blk[b] = bs;
+    for (uint32_t i = 0; i < sh.qlen; ++i) p.tqSave[(size_t)b * p.maxColl + i] = m.tq[i];
+  }
+  return cmd;
 }
 
-// Thread 0: locate the current slice and wait for the connectors, counting
-// failed polls (two-phase blocking).  Sets sh.go / sh.desc.
-__device__ __noinline__ void prepare_wait(const DaemonParams& p, Sched& sh, const Smem& m) {
-  const int b = blockIdx.x, G = p.G, K = p.K, n = p.nranks, sys = p.sysScope;
-  CtxSlot& cx = m.cache[sh.way];
-  DynCtx& d = cx.d;
-  if (d.loop >= d.nloops) { sh.go = RUN_DONE; return; }
-  const int c = sh.curId;
+// One poll of the connectors for the slice at the issue cursor (a failed poll is
+// one "spin").  On success fills `sd` and returns true.
+__device__ __forceinline__ bool try_issue(const DaemonParams& p, int b, Sched& sh, const CtxSlot& cx,
+                                          SliceDesc& sd) {
+  const int G = p.G, K = p.K, n = p.nranks, sys = p.sysScope;
+  const DynCtx& d = sh.di;
   int prim, seg;
   step_prim(d.kind, n, p.rank, cx.root, d.step, cx.s.sendbuff == cx.s.recvbuff, prim, seg);
+  const size_t cb = (size_t)sh.curId * G + b;
+  const bool needRecv = prim & A_RECV, needSend = prim & A_SEND;
+  const char* fl = p.flagsLocal + cb * kFlagStride;
+  if (needRecv && d.nrecv >= sh.headSeen) {
+    sh.headSeen = ld_relaxed(fl, sys);
+    if (d.nrecv >= sh.headSeen) return false;
+  }
+  if (needSend && d.nsent - sh.creditSeen >= (uint64_t)K) {
+    sh.creditSeen = ld_relaxed(fl + 128, sys);
+    if (d.nsent - sh.creditSeen >= (uint64_t)K) return false;
+  }
+  if (needRecv || needSend) fence_acq_rel(sys);     // acquire the peer's data / credit
   uint64_t sendOff, recvOff, len;
   seg_geom(d.kind, n, p.rank, cx.s.count, cx.s.segLen, seg, sendOff, recvOff, len);
   const int isz = elem_size(d.dtype);
@@ -476,25 +523,6 @@ __device__ __noinline__ void prepare_wait(const DaemonParams& p, Sched& sh, cons
   const uint64_t lo = laneLo + ((uint64_t)d.loop * p.slicesPerChunk + d.slc) * E;
   uint64_t hi = lo + E;
   if (hi > laneHi) hi = laneHi;
-  const size_t cb = (size_t)c * G + b;
-  const bool needRecv = prim & A_RECV, needSend = prim & A_SEND;
-  const char* fl = p.flagsLocal + cb * kFlagStride;
-  uint64_t spins = 0;
-  for (;;) {
-    bool ok = true;
-    if (needRecv && d.nrecv >= sh.headSeen) {
-      sh.headSeen = ld_relaxed(fl, sys);
-      ok = d.nrecv < sh.headSeen;
-    }
-    if (ok && needSend && d.nsent - sh.creditSeen >= (uint64_t)K) {
-      sh.creditSeen = ld_relaxed(fl + 128, sys);
-      ok = d.nsent - sh.creditSeen < (uint64_t)K;
-    }
-    if (ok) break;
-    if (++spins > sh.T) { sh.go = RUN_PREEMPT; return; }
-  }
-  if (needRecv || needSend) fence_acq_rel(sys);      // acquire the peer's data / credit
-  SliceDesc& sd = sh.desc;
   sd.src = reinterpret_cast<const char*>(cx.s.sendbuff) + (sendOff + lo) * isz;
   sd.dst = reinterpret_cast<char*>(cx.s.recvbuff) + (recvOff + lo) * isz;
   sd.cin = p.dataLocal + (cb * K + (d.nrecv % K)) * p.sliceBytes;
@@ -502,56 +530,115 @@ __device__ __noinline__ void prepare_wait(const DaemonParams& p, Sched& sh, cons
   sd.nelem = hi > lo ? (int64_t)(hi - lo) : 0;
   sd.prim = prim;
   sd.dtype = d.dtype;
-  sh.go = RUN_GO;
+  return true;
 }
 
-// Thread 0, after the block's barrier: publish the slice to the peers
-// (commit visibility) and advance the dynamic context.
-__device__ __noinline__ void commit(const DaemonParams& p, Sched& sh, const Smem& m) {
-  const int b = blockIdx.x, sys = p.sysScope;
+// Advance a (loop, step, slice) cursor by one slice of primitive `prim`.
+__device__ __forceinline__ void advance(DynCtx& d, int prim, int slicesPerChunk, int nsteps) {
+  if (prim & A_SEND) d.nsent++;
+  if (prim & A_RECV) d.nrecv++;
+  if (++d.slc == slicesPerChunk) {
+    d.slc = 0;
+    if (++d.step == nsteps) { d.step = 0; d.loop++; }
+  }
+}
+
+// Commit a slice the data warps finished: publish it to the peers (commit
+// visibility) and advance the committed dynamic context.
+__device__ __forceinline__ void commit(const DaemonParams& p, int b, Sched& sh, const Smem& m, int prim) {
+  const int sys = p.sysScope;
   CtxSlot& cx = m.cache[sh.way];
   DynCtx& d = cx.d;
-  const int prim = sh.desc.prim;
   const size_t cb = (size_t)sh.curId * p.G + b;
   if (prim & (A_RECV | A_SEND)) fence_acq_rel(sys);
-  if (prim & A_SEND) {
-    d.nsent++;
-    st_relaxed(p.flagsNext + cb * kFlagStride, d.nsent, sys);          // head of rank r+1
-  }
-  if (prim & A_RECV) {
-    d.nrecv++;
-    st_relaxed(p.flagsPrev + cb * kFlagStride + 128, d.nrecv, sys);    // credit of rank r-1
-  }
-  if (++d.slc == p.slicesPerChunk) {
-    d.slc = 0;
-    if (++d.step == cx.nsteps) { d.step = 0; d.loop++; }
-  }
+  if (prim & A_SEND) st_relaxed(p.flagsNext + cb * kFlagStride, d.nsent + 1, sys);         // head of r+1
+  if (prim & A_RECV) st_relaxed(p.flagsPrev + cb * kFlagStride + 128, d.nrecv + 1, sys);   // credit of r-1
+  advance(d, prim, p.slicesPerChunk, cx.nsteps);
   d.progressed = 1;
   m.tq[sh.pos] &= 0xffffu;                          // progressed: no longer stalled
   if (p.stickiness) {                               // raise the threshold
-    uint64_t T = sh.T * p.spinBoost;
+    const uint64_t T = sh.T * p.spinBoost;
     sh.T = T > p.spinCap ? p.spinCap : T;
   }
   p.collStats[cb].slices++;
+}
+
+// The control thread (lane 0 of warp 0): scheduler + connector protocol.  Feeds
+// slice descriptors to the data warps through the pipe, kDepth in flight.
+__device__ __noinline__ void control_main(const DaemonParams& p, int b, Sched& sh, const Smem& m, Pipe& pipe) {
+  uint32_t issued = 0, committed = 0;               // kernel-lifetime slice counters
+  for (;;) {
+    const int cmd = schedule(p, b, sh, m);
+    if (cmd == CMD_NONE) continue;
+    if (cmd == CMD_EXIT) break;
+    CtxSlot& cx = m.cache[sh.way];
+    uint64_t spins = 0;
+    int run;
+    for (;;) {
+      // retire finished slices in order
+      while (committed != issued && mbar_test(&pipe.empty[committed % kDepth], (committed / kDepth) & 1)) {
+        commit(p, b, sh, m, pipe.ring[committed % kDepth].prim);
+        ++committed;
+      }
+      if (sh.di.loop >= sh.di.nloops) {             // everything issued
+        if (committed == issued) { run = RUN_DONE; break; }
+        continue;
+      }
+      if (issued - committed == kDepth) continue;   // both buffers busy
+      SliceDesc& sd = pipe.ring[issued % kDepth];
+      if (try_issue(p, b, sh, cx, sd)) {
+        mbar_arrive(&pipe.full[issued % kDepth]);
+        ++issued;
+        advance(sh.di, sd.prim, p.slicesPerChunk, cx.nsteps);
+        spins = 0;
+      } else if (++spins > sh.T) {                  // two-phase blocking: preempt
+        while (committed != issued) {
+          mbar_wait(&pipe.empty[committed % kDepth], (committed / kDepth) & 1);
+          commit(p, b, sh, m, pipe.ring[committed % kDepth].prim);
+          ++committed;
+        }
+        run = RUN_PREEMPT;
+        break;
+      }
+    }
+    sh.lastRun = run;
+  }
+  // release the data warps
+  if (issued - committed == kDepth) {
+    mbar_wait(&pipe.empty[committed % kDepth], (committed / kDepth) & 1);
+  }
+  pipe.ring[issued % kDepth].prim = P_EXIT;
+  mbar_arrive(&pipe.full[issued % kDepth]);
 }
 
 }  // namespace
 
 // =============================================================================
 // The daemon kernel.  Launched with the largest grid/block of all collectives
-// (PAPER.md:470): grid = G blocks, one scheduler per block.
+// (PAPER.md:470): G blocks per rank, one scheduler per block.  One launch may
+// serve several ranks that live on the same device (virtual ranks): blocks
+// [i*G, (i+1)*G) run rank pp[i]'s daemon with its own SQ, CQ, contexts and
+// connectors -- the per-rank daemons are then co-resident by construction.
+//
+// Warp roles: warp 0 lane 0 is the control thread (scheduler, SQ/CQ, connector
+// flags, context switches); warps 1.. move data.  They communicate through a
+// double-buffered descriptor pipe with mbarriers, so the flag round trips and
+// fences of slice k overlap the data movement of slice k+1.
 // =============================================================================
-__global__ void __launch_bounds__(512, 1) occl_daemon_kernel(const DaemonParams* __restrict__ pp) {
-  const DaemonParams& p = *pp;
+__global__ void __launch_bounds__(512, 1) occl_daemon_kernel(const DaemonParams* __restrict__ pp, int G) {
+  const int lr = blockIdx.x / G;
+  const DaemonParams& p = pp[lr];
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ Sched sh;
+  __shared__ Pipe pipe;
   const int W = p.cacheWays;
   Smem m;
   m.cache = reinterpret_cast<CtxSlot*>(smem);
   m.cacheTag = reinterpret_cast<int*>(m.cache + W);
   m.tq = reinterpret_cast<uint32_t*>(m.cacheTag + W);
   const int tid = threadIdx.x;
-  const int b = blockIdx.x;
+  const int b = blockIdx.x - lr * G;
+  const int nDataWarps = (int)(blockDim.x >> 5) - 1;
 
   if (tid == 0) {
     const BlockState bs = p.blk[b];
@@ -565,43 +652,29 @@ __global__ void __launch_bounds__(512, 1) occl_daemon_kernel(const DaemonParams*
     for (uint32_t i = 0; i < sh.qlen; ++i) m.tq[i] = p.tqSave[(size_t)b * p.maxColl + i];
     for (int w = 0; w < W; ++w) m.cacheTag[w] = -1;
     sh.lastFetch = globaltimer();
+    for (int i = 0; i < kDepth; ++i) {
+      mbar_init(&pipe.full[i], 1);
+      mbar_init(&pipe.empty[i], nDataWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     p.blkStats[b].launches++;
   }
   __syncthreads();
 
-  for (;;) {
-    if (tid == 0) schedule(p, sh, m);
-    __syncthreads();
-    const int cmd = sh.cmd;
-    if (cmd == CMD_EXIT) break;
-    if (cmd == CMD_NONE) continue;
-
-    // context load into the shared-memory cache, 16 B per thread
-    const int way = sh.way;
-    if (sh.needLoad) {
-      if (tid < kCtxBytes / 16) {
-        const uint4* g = reinterpret_cast<const uint4*>(&p.ctx[(size_t)m.cacheTag[way] * p.G + b]);
-        reinterpret_cast<uint4*>(&m.cache[way])[tid] = ld_cg(g + tid);
-      }
-      __syncthreads();
-    }
-
-    // primitive execution, slice by slice, until preempted or done
-    for (;;) {
-      if (tid == 0) prepare_wait(p, sh, m);
-      __syncthreads();
-      const int go = sh.go;
-      if (go != RUN_GO) {
-        if (tid == 0) sh.lastRun = go;
-        break;
-      }
-      {
-        const SliceDesc sd = sh.desc;
-        move_slice_any(sd);
-      }
-      __syncthreads();
-      if (tid == 0) commit(p, sh, m);
-    }
+  if (tid < 32) {
+    if (tid == 0) control_main(p, b, sh, m, pipe);
+    return;
+  }
+  // data warps
+  const int dtid = tid - 32, dnt = (int)blockDim.x - 32;
+  const int lane = tid & 31;
+  for (uint32_t j = 0;; ++j) {
+    mbar_wait(&pipe.full[j % kDepth], (j / kDepth) & 1);
+    const SliceDesc sd = pipe.ring[j % kDepth];
+    if (sd.prim == P_EXIT) break;
+    move_slice_any(sd, dtid, dnt);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&pipe.empty[j % kDepth]);
   }
 }
 
@@ -609,15 +682,16 @@ extern "C" size_t occl_internal_daemon_smem(int maxColl, int cacheWays) {
   return (size_t)cacheWays * sizeof(CtxSlot) + (size_t)cacheWays * sizeof(int) + (size_t)(maxColl + 1) * 4 + 16;
 }
 
-// `pDev` points to a device-memory copy of the parameters (constant for the
-// communicator's lifetime); `p` is the host copy.
-extern "C" int occl_internal_launch_daemon(const DaemonParams* p, const DaemonParams* pDev, int blockThreads,
-                                           void* stream) {
+// `pDev` points to a device-memory array of `nranks` parameter blocks (one per
+// rank served by this launch, constant for the communicators' lifetime); `p` is
+// the host copy of the first (all share G, maxColl and cacheWays).
+extern "C" int occl_internal_launch_daemon(const DaemonParams* p, const DaemonParams* pDev, int nranks,
+                                           int blockThreads, void* stream) {
   const size_t smem = occl_internal_daemon_smem(p->maxColl, p->cacheWays);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(occl_daemon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
   }
-  occl_daemon_kernel<<<p->G, blockThreads, smem, (cudaStream_t)stream>>>(pDev);
+  occl_daemon_kernel<<<p->G * nranks, blockThreads, smem, (cudaStream_t)stream>>>(pDev, p->G);
   return (int)cudaGetLastError();
 }

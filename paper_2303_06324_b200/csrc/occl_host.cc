@@ -70,6 +70,30 @@ uint64_t fingerprint(const occlConfig_t& c) {
 
 }  // namespace
 
+
+namespace occl {
+// One daemon kernel launch serves every member communicator (one member unless
+// occlCommFuse merged the virtual ranks of a device).  Owns the stream, the
+// launch events and the supervisor thread (poller + event-driven restart).
+struct Launcher {
+  int dev = 0;
+  std::vector<occlComm*> members;
+  DaemonParams* paramsDev = nullptr;            // [members]
+  cudaStream_t stream = nullptr;
+  cudaEvent_t evStart = nullptr, evDone = nullptr;
+  bool launched = false;
+  uint64_t launches = 0;
+  float lastLaunchMs = 0.f;
+  uint64_t lastExitNs = 0;
+  std::mutex mu;                                 // guards launch state and members
+  std::condition_variable cv;
+  std::thread sup;
+  std::atomic<bool> stop{false};
+  std::atomic<int> autoLaunch{1};
+  std::atomic<int> sticky{0};
+};
+}  // namespace occl
+
 struct occlComm {
   int nranks = 0, rank = 0, dev = 0;
   occlConfig_t cfg{};
@@ -82,7 +106,6 @@ struct occlComm {
   uint32_t* complCnt = nullptr;
   CollStat* collStats = nullptr;
   BlockStat* blkStats = nullptr;
-  DaemonParams* paramsDev = nullptr;
   // pinned + mapped host memory
   Sqe* sqHost = nullptr;
   Sqe* sqDev = nullptr;
@@ -90,7 +113,7 @@ struct occlComm {
   uint64_t* sqCurDev = nullptr;
   uint64_t* cqHost = nullptr;
   uint64_t* cqDev = nullptr;
-  uint64_t sqTail = 0;
+  std::atomic<uint64_t> sqTail{0};
   // per-collective host state
   std::vector<uint64_t> subSeq;
   std::unique_ptr<std::atomic<int>[]> state;     // 0 idle, 1 in flight
@@ -104,19 +127,10 @@ struct occlComm {
   int sysScope = 0;
   DaemonParams params{};
   bool connected = false;
-  // daemon lifecycle
-  cudaStream_t stream = nullptr, statsStream = nullptr;
-  cudaEvent_t evStart = nullptr, evDone = nullptr;
-  bool launched = false;
-  uint64_t launches = 0;
-  float lastLaunchMs = 0.f;
-  uint64_t lastExitNs = 0;
-  std::mutex mu;
-  std::condition_variable cv;
-  std::thread sup;
-  std::atomic<bool> stop{false};
-  std::atomic<int> autoLaunch{1};
+  cudaStream_t statsStream = nullptr;
+  std::mutex sqMu;                               // single submitter: guards the SQ tail
   std::atomic<int> sticky{0};
+  occl::Launcher* L = nullptr;                   // daemon lifecycle (own, or shared after occlCommFuse)
 };
 
 namespace {
@@ -125,9 +139,9 @@ occlResult_t cuda_fail(occlComm* c, cudaError_t e) {
   if (c) c->sticky.store((int)e);
   return occlCudaError;
 }
-#define CUDACHECK(comm, call)                      \
-  do {                                             \
-    cudaError_t e_ = (call);                       \
+#define CUDACHECK(comm, call)                          \
+  do {                                                 \
+    cudaError_t e_ = (call);                           \
     if (e_ != cudaSuccess) return cuda_fail(comm, e_); \
   } while (0)
 
@@ -140,33 +154,39 @@ uint64_t min_cursor(occlComm* c) {
   return m;
 }
 
-// caller holds mu
-bool daemon_running(occlComm* c) {
-  if (!c->launched) return false;
-  cudaError_t q = cudaEventQuery(c->evDone);
+bool comm_sticky(occlComm* c) { return c->sticky.load() || (c->L && c->L->sticky.load()); }
+
+// caller holds L->mu
+bool daemon_running(Launcher* L) {
+  if (!L->launched) return false;
+  cudaError_t q = cudaEventQuery(L->evDone);
   if (q == cudaErrorNotReady) return true;
   if (q == cudaSuccess) {
     float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, c->evStart, c->evDone) == cudaSuccess) c->lastLaunchMs = ms;
-    c->launched = false;
-    c->lastExitNs = now_ns();
+    if (cudaEventElapsedTime(&ms, L->evStart, L->evDone) == cudaSuccess) L->lastLaunchMs = ms;
+    L->launched = false;
+    L->lastExitNs = now_ns();
     return false;
   }
-  c->sticky.store((int)q);
-  c->launched = false;
+  L->sticky.store((int)q);                       // asynchronous device fault: sticky
+  L->launched = false;
   return false;
 }
 
-// caller holds mu
-occlResult_t launch_locked(occlComm* c) {
-  if (c->sticky.load()) return occlCudaError;
-  if (daemon_running(c)) return occlSuccess;
-  CUDACHECK(c, cudaEventRecord(c->evStart, c->stream));
-  int e = occl_internal_launch_daemon(&c->params, c->paramsDev, c->cfg.blockThreads, c->stream);
-  if (e != 0) return cuda_fail(c, (cudaError_t)e);
-  CUDACHECK(c, cudaEventRecord(c->evDone, c->stream));
-  c->launched = true;
-  c->launches++;
+// caller holds L->mu.  One kernel launch serves every member communicator.
+occlResult_t launch_locked(Launcher* L) {
+  if (L->sticky.load()) return occlCudaError;
+  if (daemon_running(L)) return occlSuccess;
+  if (L->members.empty()) return occlInvalidUsage;
+  occlComm* c0 = L->members[0];
+  cudaError_t e;
+  if ((e = cudaEventRecord(L->evStart, L->stream)) != cudaSuccess) { L->sticky.store((int)e); return occlCudaError; }
+  int r = occl_internal_launch_daemon(&c0->params, L->paramsDev, (int)L->members.size(), c0->cfg.blockThreads,
+                                      L->stream);
+  if (r != 0) { L->sticky.store(r); return occlCudaError; }
+  if ((e = cudaEventRecord(L->evDone, L->stream)) != cudaSuccess) { L->sticky.store((int)e); return occlCudaError; }
+  L->launched = true;
+  L->launches++;
   return occlSuccess;
 }
 
@@ -183,31 +203,76 @@ bool try_complete(occlComm* c, int id) {
 }
 
 // Supervisor: poller + callback map + event-driven (re)start.
-void supervisor_main(occlComm* c) {
-  cudaSetDevice(c->dev);
-  uint64_t backoffNs = 50'000;
-  while (!c->stop.load()) {
-    bool pending;
+void supervisor_main(Launcher* L) {
+  cudaSetDevice(L->dev);
+  const uint64_t backoffNs = 50'000;
+  std::vector<occlComm*> ms;
+  while (!L->stop.load()) {
+    bool pending = false;
     {
-      std::lock_guard<std::mutex> lk(c->mu);
-      const bool newSqe = c->sqTail > min_cursor(c);
-      pending = newSqe || c->inflight.load() > 0;
-      if (c->autoLaunch.load() && pending && !daemon_running(c) && !c->sticky.load()) {
+      std::lock_guard<std::mutex> lk(L->mu);
+      ms = L->members;
+      bool newSqe = false;
+      for (occlComm* c : ms) {
+        if (c->sqTail.load() > min_cursor(c)) newSqe = true;
+        if (c->inflight.load() > 0) pending = true;
+      }
+      pending = pending || newSqe;
+      if (L->autoLaunch.load() && pending && !daemon_running(L) && !L->sticky.load()) {
         // new SQEs start the daemon at once; collectives that are merely stuck
         // (the daemon quit voluntarily) restart after a back-off so that device
         // synchronisation on the host can complete in between
-        if (newSqe || now_ns() - c->lastExitNs > backoffNs) launch_locked(c);
+        if (newSqe || now_ns() - L->lastExitNs > backoffNs) launch_locked(L);
       }
     }
-    for (int id = 0; id < c->cfg.maxColl && c->inflight.load() > 0; ++id)
-      if (c->cb[id] && c->state[id].load() == 1) try_complete(c, id);
+    for (occlComm* c : ms)
+      for (int id = 0; id < c->cfg.maxColl && c->inflight.load() > 0; ++id)
+        if (c->cb[id] && c->state[id].load() == 1) try_complete(c, id);
     if (!pending) {
-      std::unique_lock<std::mutex> lk(c->mu);
-      c->cv.wait_for(lk, std::chrono::milliseconds(5));
+      std::unique_lock<std::mutex> lk(L->mu);
+      L->cv.wait_for(lk, std::chrono::milliseconds(5));
     } else {
       std::this_thread::sleep_for(std::chrono::microseconds(20));
     }
   }
+}
+
+occlResult_t launcher_start(Launcher* L, const std::vector<occlComm*>& members) {
+  L->dev = members[0]->dev;
+  L->members = members;
+  cudaSetDevice(L->dev);
+  std::vector<DaemonParams> ps;
+  for (occlComm* c : members) ps.push_back(c->params);
+  if (cudaMalloc(&L->paramsDev, ps.size() * sizeof(DaemonParams)) != cudaSuccess) return occlCudaError;
+  if (cudaMemcpy(L->paramsDev, ps.data(), ps.size() * sizeof(DaemonParams), cudaMemcpyHostToDevice) != cudaSuccess)
+    return occlCudaError;
+  if (cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking) != cudaSuccess) return occlCudaError;
+  if (cudaEventCreate(&L->evStart) != cudaSuccess) return occlCudaError;
+  if (cudaEventCreate(&L->evDone) != cudaSuccess) return occlCudaError;
+  L->autoLaunch.store(members[0]->cfg.autoLaunch ? 1 : 0);
+  try {
+    L->sup = std::thread(supervisor_main, L);
+  } catch (...) {
+    return occlSystemError;
+  }
+  for (occlComm* c : members) c->L = L;
+  return occlSuccess;
+}
+
+// Stop the supervisor and wait for the daemon to be idle; frees the launcher.
+void launcher_stop(Launcher* L) {
+  L->stop.store(true);
+  L->cv.notify_all();
+  if (L->sup.joinable()) L->sup.join();
+  cudaSetDevice(L->dev);
+  if (L->launched) cudaEventSynchronize(L->evDone);
+  if (L->paramsDev) cudaFree(L->paramsDev);
+  if (L->evStart) cudaEventDestroy(L->evStart);
+  if (L->evDone) cudaEventDestroy(L->evDone);
+  if (L->stream) cudaStreamDestroy(L->stream);
+  for (occlComm* c : L->members)
+    if (c->L == L) c->L = nullptr;
+  delete L;
 }
 
 occlResult_t validate_config(const occlConfig_t& c) {
@@ -240,34 +305,45 @@ int coll_blocks(const occlComm* c, int kind, size_t count, int dtype) {
   return (int)nb;
 }
 
+void write_sqe(occlComm* c, Sqe& e) {
+  const uint64_t t = c->sqTail.load();
+  Sqe* s = &c->sqHost[t % c->cfg.sqDepth];
+  std::memcpy(reinterpret_cast<char*>(s) + 8, reinterpret_cast<const char*>(&e) + 8, sizeof(Sqe) - 8);
+  std::atomic_thread_fence(std::memory_order_release);
+  reinterpret_cast<std::atomic<uint64_t>*>(&s->seq)->store(t + 1, std::memory_order_release);
+  c->sqTail.store(t + 1);
+}
+
 occlResult_t push_sqe(occlComm* c, Sqe& e, bool launchNow) {
-  std::unique_lock<std::mutex> lk(c->mu);
+  Launcher* L = c->L;
+  std::unique_lock<std::mutex> lk(c->sqMu);
   // wait for a free slot: the daemon always drains the SQ (invariant I4)
-  while (c->sqTail - min_cursor(c) >= (uint64_t)c->cfg.sqDepth) {
-    if (c->sticky.load()) return occlCudaError;
-    if (c->autoLaunch.load() && !daemon_running(c)) launch_locked(c);
+  while (c->sqTail.load() - min_cursor(c) >= (uint64_t)c->cfg.sqDepth) {
+    if (comm_sticky(c)) return occlCudaError;
+    if (L->autoLaunch.load()) {
+      std::lock_guard<std::mutex> g(L->mu);
+      if (!daemon_running(L)) launch_locked(L);
+    }
     lk.unlock();
     std::this_thread::yield();
     lk.lock();
   }
-  Sqe* s = &c->sqHost[c->sqTail % c->cfg.sqDepth];
-  e.seq = 0;
-  std::memcpy(reinterpret_cast<char*>(s) + 8, reinterpret_cast<const char*>(&e) + 8, sizeof(Sqe) - 8);
-  std::atomic_thread_fence(std::memory_order_release);
-  reinterpret_cast<std::atomic<uint64_t>*>(&s->seq)->store(c->sqTail + 1, std::memory_order_release);
-  c->sqTail++;
-  occlResult_t r = occlSuccess;
-  if (launchNow && c->autoLaunch.load() && !daemon_running(c)) r = launch_locked(c);
+  write_sqe(c, e);
   lk.unlock();
-  c->cv.notify_one();
+  occlResult_t r = occlSuccess;
+  if (launchNow && L->autoLaunch.load()) {       // the first SQE starts the daemon
+    std::lock_guard<std::mutex> g(L->mu);
+    if (!daemon_running(L)) r = launch_locked(L);
+  }
+  L->cv.notify_one();
   return r;
 }
 
 occlResult_t submit(occlComm* c, int kind, int dtype, int op, int root, size_t count, const void* send,
                     void* recv, int collId) {
   if (!c) return occlInvalidArgument;
-  if (!c->connected) return occlInvalidUsage;
-  if (c->sticky.load()) return occlCudaError;
+  if (!c->connected || !c->L) return occlInvalidUsage;
+  if (comm_sticky(c)) return occlCudaError;
   if (collId < 0) return occlInvalidArgument;
   if (collId >= c->cfg.maxColl) return occlRegistryFull;
   if (dtype < 0 || dtype > 2) return occlInvalidArgument;
@@ -297,7 +373,7 @@ occlResult_t submit(occlComm* c, int kind, int dtype, int op, int root, size_t c
   return push_sqe(c, e, true);
 }
 
-void free_all(occlComm* c) {
+void free_comm(occlComm* c) {
   if (c->nextIpc && c->nextArena) cudaIpcCloseMemHandle(c->nextArena);
   if (c->prevIpc && c->prevArena && c->prevArena != c->nextArena) cudaIpcCloseMemHandle(c->prevArena);
   if (c->arena) cudaFree(c->arena);
@@ -307,13 +383,9 @@ void free_all(occlComm* c) {
   if (c->complCnt) cudaFree(c->complCnt);
   if (c->collStats) cudaFree(c->collStats);
   if (c->blkStats) cudaFree(c->blkStats);
-  if (c->paramsDev) cudaFree(c->paramsDev);
   if (c->sqHost) cudaFreeHost(c->sqHost);
   if (c->sqCurHost) cudaFreeHost(c->sqCurHost);
   if (c->cqHost) cudaFreeHost(c->cqHost);
-  if (c->evStart) cudaEventDestroy(c->evStart);
-  if (c->evDone) cudaEventDestroy(c->evDone);
-  if (c->stream) cudaStreamDestroy(c->stream);
   if (c->statsStream) cudaStreamDestroy(c->statsStream);
 }
 
@@ -393,7 +465,7 @@ occlResult_t occlCommCreate(occlComm_t* out, int nranks, int rank, int cudaDev, 
   c->cb.assign(M, nullptr);
   c->cbArg.assign(M, nullptr);
   occlComm* cp = c.get();
-  auto fail = [&](cudaError_t e) { free_all(cp); (void)e; return occlCudaError; };
+  auto fail = [&](cudaError_t) { free_comm(cp); return occlCudaError; };
   cudaError_t e;
   if ((e = cudaSetDevice(cudaDev)) != cudaSuccess) return fail(e);
   if ((e = cudaMalloc(&cp->arena, c->dataBytes + c->flagsBytes)) != cudaSuccess) return fail(e);
@@ -409,7 +481,6 @@ occlResult_t occlCommCreate(occlComm_t* out, int nranks, int rank, int cudaDev, 
   if ((e = cudaMemset(cp->collStats, 0, M * G * sizeof(CollStat))) != cudaSuccess) return fail(e);
   if ((e = cudaMalloc(&cp->blkStats, G * sizeof(BlockStat))) != cudaSuccess) return fail(e);
   if ((e = cudaMemset(cp->blkStats, 0, G * sizeof(BlockStat))) != cudaSuccess) return fail(e);
-  if ((e = cudaMalloc(&cp->paramsDev, sizeof(DaemonParams))) != cudaSuccess) return fail(e);
   const unsigned flags = cudaHostAllocMapped | cudaHostAllocPortable;
   if ((e = cudaHostAlloc(&cp->sqHost, cfg.sqDepth * sizeof(Sqe), flags)) != cudaSuccess) return fail(e);
   std::memset(cp->sqHost, 0, cfg.sqDepth * sizeof(Sqe));
@@ -420,12 +491,8 @@ occlResult_t occlCommCreate(occlComm_t* out, int nranks, int rank, int cudaDev, 
   if ((e = cudaHostAlloc(&cp->cqHost, M * sizeof(uint64_t), flags)) != cudaSuccess) return fail(e);
   std::memset(cp->cqHost, 0, M * sizeof(uint64_t));
   if ((e = cudaHostGetDevicePointer(&cp->cqDev, cp->cqHost, 0)) != cudaSuccess) return fail(e);
-  if ((e = cudaStreamCreateWithFlags(&cp->stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
   if ((e = cudaStreamCreateWithFlags(&cp->statsStream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
-  if ((e = cudaEventCreate(&cp->evStart)) != cudaSuccess) return fail(e);
-  if ((e = cudaEventCreate(&cp->evDone)) != cudaSuccess) return fail(e);
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(e);
-  cp->autoLaunch.store(cfg.autoLaunch ? 1 : 0);
   *out = c.release();
   return occlSuccess;
 }
@@ -447,9 +514,7 @@ occlResult_t occlCommGetHandle(occlComm_t c, void* out, size_t* len) {
   h.cfgFingerprint = fingerprint(c->cfg);
   cudaSetDevice(c->dev);
   if (cudaIpcGetMemHandle(&h.ipc, c->arena) != cudaSuccess) {
-    // IPC may be unavailable (e.g. some virtualised setups); same-process peers
-    // do not need it.
-    cudaGetLastError();
+    cudaGetLastError();     // same-process peers do not need IPC
   }
   std::memcpy(out, &h, sizeof(h));
   *len = sizeof(h);
@@ -537,15 +602,39 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   p.idleSleepNs = c->cfg.idleSleepNs;
   p.cacheWays = c->cfg.cacheWays;
   p.sysScope = c->sysScope;
-  CUDACHECK(c, cudaMemcpy(c->paramsDev, &p, sizeof(p), cudaMemcpyHostToDevice));
-  c->connected = true;
-  try {
-    c->sup = std::thread(supervisor_main, c);
-  } catch (...) {
-    c->connected = false;
-    return occlSystemError;
+  Launcher* L = new Launcher();
+  if ((r = launcher_start(L, {c})) != occlSuccess) {
+    launcher_stop(L);
+    return r;
   }
+  c->connected = true;
   return occlSuccess;
+}
+
+occlResult_t occlCommFuse(occlComm_t* comms, int n) {
+  if (!comms || n < 1) return occlInvalidArgument;
+  std::vector<occlComm*> ms(comms, comms + n);
+  for (occlComm* c : ms) {
+    if (!c || !c->connected || !c->L) return occlInvalidUsage;
+    if (c->dev != ms[0]->dev || c->cfg.gridBlocks != ms[0]->cfg.gridBlocks ||
+        c->cfg.maxColl != ms[0]->cfg.maxColl || c->cfg.cacheWays != ms[0]->cfg.cacheWays ||
+        c->cfg.blockThreads != ms[0]->cfg.blockThreads)
+      return occlInvalidArgument;
+    if (c->L->members.size() != 1) return occlInvalidUsage;   // fuse single-member launchers only
+    if (c->inflight.load() > 0) return occlInvalidUsage;
+  }
+  for (occlComm* c : ms) {
+    Launcher* old = c->L;
+    {
+      std::lock_guard<std::mutex> lk(old->mu);
+      if (daemon_running(old)) return occlInvalidUsage;
+    }
+  }
+  for (occlComm* c : ms) launcher_stop(c->L);
+  Launcher* L = new Launcher();
+  occlResult_t r = launcher_start(L, ms);
+  if (r != occlSuccess) launcher_stop(L);
+  return r;
 }
 
 occlResult_t occlCommInit(occlComm_t* out, int nranks, int rank, int cudaDev, occlAllGatherFn ag, void* agCtx,
@@ -569,25 +658,38 @@ occlResult_t occlCommDestroy(occlComm_t c) {
     for (int id = 0; id < c->cfg.maxColl; ++id) try_complete(c, id);
     if (c->inflight.load() > 0) return occlInvalidUsage;
   }
-  c->stop.store(true);
-  c->cv.notify_all();
-  if (c->sup.joinable()) c->sup.join();
   cudaSetDevice(c->dev);
-  {
-    std::lock_guard<std::mutex> lk(c->mu);
-    if (c->connected && daemon_running(c)) {
-      // Exiting SQE: the daemon drains and exits
-      Sqe e{};
-      e.kind = kExit;
-      Sqe* s = &c->sqHost[c->sqTail % c->cfg.sqDepth];
-      std::memcpy(reinterpret_cast<char*>(s) + 8, reinterpret_cast<const char*>(&e) + 8, sizeof(Sqe) - 8);
-      std::atomic_thread_fence(std::memory_order_release);
-      reinterpret_cast<std::atomic<uint64_t>*>(&s->seq)->store(c->sqTail + 1, std::memory_order_release);
-      c->sqTail++;
+  Launcher* L = c->L;
+  if (L) {
+    {
+      std::lock_guard<std::mutex> lk(L->mu);
+      if (daemon_running(L)) {
+        // Exiting SQE to every member: the daemon drains and exits
+        for (occlComm* m : L->members) {
+          Sqe e{};
+          e.kind = kExit;
+          std::lock_guard<std::mutex> g(m->sqMu);
+          write_sqe(m, e);
+        }
+      }
+    }
+    if (L->members.size() <= 1) {
+      launcher_stop(L);
+    } else {
+      // a fused member leaves: relaunch-capable launcher keeps serving the others
+      L->stop.store(true);
+      L->cv.notify_all();
+      if (L->sup.joinable()) L->sup.join();
+      if (L->launched) cudaEventSynchronize(L->evDone);
+      std::vector<occlComm*> rest;
+      for (occlComm* m : L->members)
+        if (m != c) rest.push_back(m);
+      launcher_stop(L);
+      Launcher* L2 = new Launcher();
+      if (launcher_start(L2, rest) != occlSuccess) launcher_stop(L2);
     }
   }
-  if (c->launched) cudaEventSynchronize(c->evDone);
-  free_all(c);
+  free_comm(c);
   delete c;
   return occlSuccess;
 }
@@ -613,7 +715,7 @@ occlResult_t occlTest(occlComm_t c, int id, int* done) {
   if (c->subSeq[id] == 0) return occlUnknownId;
   if (c->state[id].load() == 1) try_complete(c, id);
   *done = c->state[id].load() == 0;
-  if (!*done && c->sticky.load()) return occlCudaError;
+  if (!*done && comm_sticky(c)) return occlCudaError;
   return occlSuccess;
 }
 
@@ -627,11 +729,11 @@ occlResult_t occlWait(occlComm_t c, int id, int64_t timeoutNs) {
     if (c->state[id].load(std::memory_order_acquire) == 0) return occlSuccess;
     if (try_complete(c, id)) return occlSuccess;
     if (c->state[id].load() == 0) return occlSuccess;
-    if (c->sticky.load()) return occlCudaError;
+    if (comm_sticky(c)) return occlCudaError;
     if ((++it & 1023) == 0) {
-      {
-        std::lock_guard<std::mutex> lk(c->mu);
-        daemon_running(c);                       // surfaces asynchronous device faults
+      if (c->L) {
+        std::lock_guard<std::mutex> lk(c->L->mu);
+        daemon_running(c->L);                    // surfaces asynchronous device faults
       }
       if (timeoutNs >= 0 && now_ns() - t0 > (uint64_t)timeoutNs) return occlTimeout;
       std::this_thread::yield();
@@ -673,10 +775,12 @@ occlResult_t occlGetStats(occlComm_t c, occlStats_t* out) {
     out->ctxSaves += s.ctxSaves;
     out->slices += s.slices;
   }
-  std::lock_guard<std::mutex> lk(c->mu);
-  daemon_running(c);
-  out->launches = c->launches;
-  out->lastLaunchMs = c->lastLaunchMs;
+  if (c->L) {
+    std::lock_guard<std::mutex> lk(c->L->mu);
+    daemon_running(c->L);
+    out->launches = c->L->launches;
+    out->lastLaunchMs = c->L->lastLaunchMs;
+  }
   return occlSuccess;
 }
 
@@ -702,7 +806,7 @@ occlResult_t occlGetCollStats(occlComm_t c, int id, occlCollStats_t* out) {
 
 occlResult_t occlCommExit(occlComm_t c) {
   if (!c) return occlInvalidArgument;
-  if (!c->connected) return occlInvalidUsage;
+  if (!c->connected || !c->L) return occlInvalidUsage;
   Sqe e{};
   e.kind = kExit;
   return push_sqe(c, e, true);
@@ -710,26 +814,26 @@ occlResult_t occlCommExit(occlComm_t c) {
 
 occlResult_t occlCommLaunch(occlComm_t c) {
   if (!c) return occlInvalidArgument;
-  if (!c->connected) return occlInvalidUsage;
+  if (!c->connected || !c->L) return occlInvalidUsage;
   cudaSetDevice(c->dev);
-  std::lock_guard<std::mutex> lk(c->mu);
-  return launch_locked(c);
+  std::lock_guard<std::mutex> lk(c->L->mu);
+  return launch_locked(c->L);
 }
 
 occlResult_t occlCommSetAutoLaunch(occlComm_t c, int enable) {
-  if (!c) return occlInvalidArgument;
-  c->autoLaunch.store(enable ? 1 : 0);
-  c->cv.notify_one();
+  if (!c || !c->L) return occlInvalidArgument;
+  c->L->autoLaunch.store(enable ? 1 : 0);
+  c->L->cv.notify_one();
   return occlSuccess;
 }
 
 occlResult_t occlCommQuiesce(occlComm_t c, int64_t timeoutNs) {
-  if (!c) return occlInvalidArgument;
+  if (!c || !c->L) return occlInvalidArgument;
   const uint64_t t0 = now_ns();
   for (;;) {
     {
-      std::lock_guard<std::mutex> lk(c->mu);
-      if (!daemon_running(c)) return c->sticky.load() ? occlCudaError : occlSuccess;
+      std::lock_guard<std::mutex> lk(c->L->mu);
+      if (!daemon_running(c->L)) return comm_sticky(c) ? occlCudaError : occlSuccess;
     }
     if (timeoutNs >= 0 && now_ns() - t0 > (uint64_t)timeoutNs) return occlTimeout;
     std::this_thread::sleep_for(std::chrono::microseconds(10));
@@ -737,8 +841,8 @@ occlResult_t occlCommQuiesce(occlComm_t c, int64_t timeoutNs) {
 }
 
 occlResult_t occlCommGetStream(occlComm_t c, void** stream) {
-  if (!c || !stream) return occlInvalidArgument;
-  *stream = (void*)c->stream;
+  if (!c || !stream || !c->L) return occlInvalidArgument;
+  *stream = (void*)c->L->stream;
   return occlSuccess;
 }
 

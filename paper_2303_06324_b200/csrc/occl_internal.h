@@ -113,5 +113,5 @@ struct DaemonParams {
 
 // Launch entry implemented in occl_daemon.cu (internal, not part of the C-ABI).
 extern "C" int occl_internal_launch_daemon(const occl::DaemonParams* p, const occl::DaemonParams* pDev,
-                                           int blockThreads, void* stream);
+                                           int nranks, int blockThreads, void* stream);
 extern "C" size_t occl_internal_daemon_smem(int maxColl, int cacheWays);

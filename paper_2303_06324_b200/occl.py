@@ -34,7 +34,7 @@ EXPORTED = [
     "occlCommInit", "occlCommDestroy", "occlAllReduce", "occlAllGather", "occlReduceScatter",
     "occlBroadcast", "occlWait", "occlTest", "occlSetCallback", "occlGetStats", "occlGetCollStats",
     "occlCommExit", "occlCommLaunch", "occlCommSetAutoLaunch", "occlCommQuiesce", "occlCommGetStream",
-    "occlCollBlocks",
+    "occlCollBlocks", "occlCommFuse",
 ]
 
 
@@ -103,6 +103,7 @@ def _lib():
             "occlCommQuiesce": [vp, i64],
             "occlCommGetStream": [vp, C.POINTER(vp)],
             "occlCollBlocks": [vp, i, sz, i, C.POINTER(i)],
+            "occlCommFuse": [C.POINTER(vp), i],
         }.items():
             f = getattr(L, name)
             f.restype = C.c_int
@@ -316,15 +317,24 @@ def _dt(t):
     return {torch.float32: occlFloat32, torch.bfloat16: occlBfloat16, torch.int32: occlInt32}[t.dtype]
 
 
-def local_group(nranks, device=0, cfg=None, **overrides):
-    """A ring of `nranks` virtual ranks in this process on one device (each rank its
-    own communicator, daemon kernel and stream).  Connectors are plain HBM."""
+def occlCommFuse(comms):
+    arr = (C.c_void_p * len(comms))(*[c.h if isinstance(c, Comm) else c for c in comms])
+    check(_lib().occlCommFuse(arr, len(comms)), "occlCommFuse")
+
+
+def local_group(nranks, device=0, cfg=None, fuse=True, **overrides):
+    """A ring of `nranks` virtual ranks in this process on one device.  Each rank is
+    its own communicator (SQ, CQ, contexts, connectors in plain HBM); with
+    fuse=True one daemon kernel launch serves all of them (occlCommFuse)."""
     cfg = cfg if cfg is not None else occlConfigDefault(**overrides)
     hs = [occlCommCreate(nranks, r, device, cfg) for r in range(nranks)]
     handles = [occlCommGetHandle(h) for h in hs]
     for h in hs:
         occlCommConnect(h, handles)
-    return [Comm(h, nranks, r, device, cfg) for r, h in enumerate(hs)]
+    comms = [Comm(h, nranks, r, device, cfg) for r, h in enumerate(hs)]
+    if fuse and nranks > 1:
+        occlCommFuse(comms)
+    return comms
 
 
 def process_group(pg=None, device=None, cfg=None, **overrides):
