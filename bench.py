@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--slice-kib", type=int, default=64)
     ap.add_argument("--conn-slots", type=int, default=4)
     ap.add_argument("--slices-per-chunk", type=int, default=2)
+    ap.add_argument("--threads", type=int, default=544)
+    ap.add_argument("--pipe-depth", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--check", action="store_true", help="sampled oracle check of the timed output")
@@ -197,6 +199,7 @@ def make_ring(args, world, prank, dev, dist):
     V = R // world
     cfg = occl.occlConfigDefault(gridBlocks=args.grid_blocks, sliceBytes=args.slice_kib * 1024,
                                  connSlots=args.conn_slots, slicesPerChunk=args.slices_per_chunk,
+                                 blockThreads=args.threads, pipeDepth=args.pipe_depth,
                                  maxColl=128, autoLaunch=0)
     hs = [occl.occlCommCreate(R, prank * V + i, dev, cfg) for i in range(V)]
     mine = [occl.occlCommGetHandle(h) for h in hs]
@@ -265,6 +268,7 @@ def run_occl(args):
     barrier()
     torch.cuda.synchronize()
     before = [c.stats() for c in comms]
+    pb = [c.probes() for c in comms]
     ms_total, launches, left = 0.0, 0, args.steps
     with ClockSampler(dev) as clk:
         while left > 0:
@@ -275,6 +279,14 @@ def run_occl(args):
     torch.cuda.synchronize()
     barrier()
     after = [c.stats() for c in comms]
+    pa = [c.probes() for c in comms]
+    probes = {k: sum(a[k] - b[k] for a, b in zip(pa, pb)) for k in pa[0]}
+    nc, nd = max(1, probes["nCommit"]), max(1, probes["nData"])
+    probe_summary = {"per_commit_cycles": {k: round(probes[k] / nc, 1) for k in
+                                           ("cycRun", "cycPoll", "cycAcqFence", "cycRelFence")},
+                     "per_slice_data_cycles": round(probes["cycData"] / nd, 1),
+                     "per_slice_datawait_cycles": round(probes["cycDataWait"] / nd, 1),
+                     "commits": probes["nCommit"], "data_slices_timed": probes["nData"]}
     if dist is not None:
         t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -386,13 +398,15 @@ def run_occl(args):
                                f"{V} rank(s) per GPU" + (" (virtual ranks, one fused daemon)" if V > 1 else ""),
                    "ranks": R, "ranks_per_gpu": V, "size_bytes_per_rank": size, "grid_blocks": args.grid_blocks,
                    "slice_bytes": args.slice_kib * 1024, "conn_slots": args.conn_slots,
-                   "slices_per_chunk": args.slices_per_chunk, "l2": "inputs larger than L2 (R x S >> 126 MB)",
+                   "slices_per_chunk": args.slices_per_chunk, "block_threads": args.threads,
+                   "pipe_depth": args.pipe_depth, "l2": "inputs larger than L2 (R x S >> 126 MB)",
                    "algbw_GBps": size / (ms_step / 1e3) / 1e9},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "probes": probe_summary,
         "daemon": {"slices": slices, "preemptions": sum(a["preemptions"] - b["preemptions"] for a, b in zip(after, before)),
                    "cqe": sum(a["cqeWritten"] - b["cqeWritten"] for a, b in zip(after, before))},
     }

@@ -75,7 +75,7 @@ typedef enum { occlOrderFifo = 0, occlOrderPriority = 1 } occlOrderPolicy_t;
 typedef struct {
   int maxColl;            /* registry size: collId in [0, maxColl) ("up to 1,000")   */
   int gridBlocks;         /* G: daemon grid = max blocks any collective uses        */
-  int blockThreads;       /* threads per daemon block (multiple of 32, <= 1024)                    */
+  int blockThreads;       /* threads per block: 1 control warp + data warps (multiple of 32, 64..544) */
   int connSlots;          /* K: slots per connector; must exceed slicesPerChunk                    */
   int slicesPerChunk;     /* slices each primitive moves per loop             */
   size_t sliceBytes;      /* bytes per connector slot (multiple of 16)                             */
@@ -95,6 +95,7 @@ typedef struct {
   uint32_t idleSleepNs;   /* back-off between empty SQ polls                                       */
   int autoLaunch;         /* 1 = event-driven (re)start by the host supervisor */
   int cacheWays;          /* direct-mapped shared-memory context cache ways        */
+  int pipeDepth;          /* slices in flight between the control warp and the data warps (1..8)   */
 } occlConfig_t;
 
 /* Aggregate counters (device counters summed over blocks/collectives). */
@@ -114,6 +115,20 @@ typedef struct {
 typedef struct {
   uint64_t preemptions, ctxLoads, ctxSaves, slices, completions;
 } occlCollStats_t;
+
+/* In-kernel timing probes summed over the communicator's blocks, in SM clock
+ * cycles (the paper's "core execution time" probes).  Values
+ * accumulate over daemon launches; each block flushes them when it exits. */
+typedef struct {
+  uint64_t cycRun;        /* control thread inside collective runs                  */
+  uint64_t cycPoll;       /* ... in failed connector polls (waiting for peers)      */
+  uint64_t cycAcqFence;   /* ... in the acquire fence after a successful poll       */
+  uint64_t cycRelFence;   /* ... in the commit (release) fence                      */
+  uint64_t cycData;       /* data-group leader threads moving slices                */
+  uint64_t cycDataWait;   /* data-group leader threads waiting for a descriptor     */
+  uint64_t nData;         /* slices timed by data-group leaders                     */
+  uint64_t nCommit;       /* slices committed                                       */
+} occlProbes_t;
 
 /* Bootstrap all-gather: gather `bytesPerRank` bytes from every rank into `out`
  * (rank-major).  Return 0 on success. */
@@ -185,6 +200,7 @@ occlResult_t occlSetCallback(occlComm_t comm, int collId, occlCallback_t cb, voi
 /* Counters (a snapshot; the daemon may be running). */
 occlResult_t occlGetStats(occlComm_t comm, occlStats_t* out);
 occlResult_t occlGetCollStats(occlComm_t comm, int collId, occlCollStats_t* out);
+occlResult_t occlGetProbes(occlComm_t comm, occlProbes_t* out);
 
 /* --- daemon control (the paper's lifecycle made explicit) --------------------- */
 /* Push an Exiting SQE: every block drains its task queue, then exits.  A later

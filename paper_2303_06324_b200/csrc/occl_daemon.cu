@@ -56,6 +56,12 @@ __device__ __forceinline__ void st_relaxed(void* p, uint64_t v, int sys) {
   if (sys) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
   else     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
+// Monotonic publication of a connector counter: slices are published by whichever
+// data warp finishes last, so two publications may race; max keeps it monotonic.
+__device__ __forceinline__ void red_max_relaxed(void* p, uint64_t v, int sys) {
+  if (sys) asm volatile("red.relaxed.sys.global.max.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+  else     asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void st_volatile_u64(volatile uint64_t* p, uint64_t v) {
   asm volatile("st.volatile.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
@@ -132,6 +138,9 @@ struct SliceDesc {
   const char* cin;     // recv connector slot
   char* dst;           // recv-buffer slice
   char* cout;          // downstream connector slot
+  char* headOut;       // downstream head flag (published = headVal) when prim sends
+  char* creditOut;     // upstream credit flag (published = creditVal) when prim receives
+  uint64_t headVal, creditVal;
   int64_t nelem;
   int prim;
   int dtype;
@@ -153,14 +162,16 @@ template <> __device__ __forceinline__ uint16_t sadd<kBF16>(uint16_t a, uint16_t
   return __bfloat16_as_ushort(__hadd(x, y));
 }
 
-// Move one slice with all threads of the block: 128-bit vectors, U independent
-// loads in flight per thread, then the stores.  The action
-// bits are warp-uniform runtime flags; only the element type is a template.
+// Move one slice with the data warps: 128-bit vectors, U independent loads in
+// flight per thread (twice that for reduce), then the stores.
+// Loads bypass L1 (ld.global.cg): connector slots are rewritten by peers and the
+// persistent kernel must never see a stale line.  The action bits are
+// warp-uniform runtime flags; only the element type is a template.
 template <int DT>
 __device__ __forceinline__ void move_slice(const SliceDesc& d, const int tid, const int nt) {
   typedef typename Elem<DT>::T T;
   constexpr int A = 16 / sizeof(T);
-  constexpr int U = 4;
+  constexpr int U = 8;
   const int prim = d.prim;
   const bool recv = prim & A_RECV, reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
   const int n = (int)d.nelem;                     // <= sliceBytes / sizeof(T)
@@ -171,26 +182,34 @@ __device__ __forceinline__ void move_slice(const SliceDesc& d, const int tid, co
   const uint4* vi = reinterpret_cast<const uint4*>(recv ? d.cin : d.src);
   uint4* vd = reinterpret_cast<uint4*>(d.dst);
   uint4* vo = reinterpret_cast<uint4*>(d.cout);
-  for (int base = tid; base < nvec; base += U * nt) {
-    uint4 a[U], b[U];
+  int i = tid;
+  // full tiles: U vectors per thread, no bounds checks
+  for (; i + (U - 1) * nt < nvec; i += U * nt) {
+    uint4 a[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = base + u * nt;
-      if (i < nvec) {
-        a[u] = ld_cg(vi + i);
-        if (reduce) b[u] = ld_cg(vs + i);
-      }
-    }
+    for (int u = 0; u < U; ++u) a[u] = __ldcg(vi + i + u * nt);
+    if (reduce) {
+      uint4 c[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = base + u * nt;
-      if (i < nvec) {
-        uint4 v = a[u];
-        if (reduce) v = vadd<DT>(a[u], b[u]);
-        if (copy) st_v4(vd + i, v);
-        if (send) st_cg_v4(vo + i, v);
-      }
+      for (int u = 0; u < U; ++u) c[u] = __ldcg(vs + i + u * nt);
+#pragma unroll
+      for (int u = 0; u < U; ++u) a[u] = vadd<DT>(a[u], c[u]);
     }
+    if (copy) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) __stcg(vd + i + u * nt, a[u]);
+    }
+    if (send) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) __stcg(vo + i + u * nt, a[u]);
+    }
+  }
+  // remaining vectors, one per thread per iteration
+  for (; i < nvec; i += nt) {
+    uint4 v = __ldcg(vi + i);
+    if (reduce) v = vadd<DT>(v, __ldcg(vs + i));
+    if (copy) __stcg(vd + i, v);
+    if (send) __stcg(vo + i, v);
   }
   // scalar tail (ragged segment ends) or the whole slice when misaligned
   const T* ss = reinterpret_cast<const T*>(d.src);
@@ -198,8 +217,8 @@ __device__ __forceinline__ void move_slice(const SliceDesc& d, const int tid, co
   T* sd = reinterpret_cast<T*>(d.dst);
   T* so = reinterpret_cast<T*>(d.cout);
   for (int e = nvec * A + tid; e < n; e += nt) {
-    T v = ld_cg_scalar(si + e);
-    if (reduce) v = sadd<DT>(v, ld_cg_scalar(ss + e));
+    T v = __ldcg(si + e);
+    if (reduce) v = sadd<DT>(v, __ldcg(ss + e));
     if (copy) sd[e] = v;
     if (send) so[e] = v;
   }
@@ -292,7 +311,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 enum : int { CMD_NONE = 0, CMD_RUN = 1, CMD_EXIT = 2 };
 enum : int { RUN_PREEMPT = 0, RUN_GO = 1, RUN_DONE = 2 };
 constexpr int P_EXIT = 0x100;          // descriptor telling the data warps to leave
-constexpr int kDepth = 2;              // slices in flight between control and data warps
+constexpr int kMaxDepth = 8;           // max slices in flight between control and data warps
+constexpr int kMaxBlockThreads = 544;  // 1 control warp + up to 16 data warps
 
 // Scheduler state of one block; touched only by the control thread.
 struct Sched {
@@ -301,16 +321,19 @@ struct Sched {
   uint32_t qlen, pos, exiting;
   int lastRun, curId;
   int way;
-  DynCtx di;                            // issue cursor (runs ahead of the committed cx.d)
+  unsigned long long cycRun, cycPoll, cycAcqFence, cycRelFence, nCommit;   // probes
 };
 
-// Control -> data warp pipeline: slice descriptors in a ring of kDepth buffers;
-// full[i] completes when the control thread published ring[i], empty[i] when
-// every data warp finished moving it.
+// Control -> data warp pipeline: slice descriptors in a ring of `depth` buffers.
+// full[i] completes when the control thread published ring[i]; the data warp
+// that finishes slot i LAST publishes the slice to the peers (release fence +
+// head / credit store) and completes empty[i].  All data warps move slices in
+// order, so slices are published in order and the counters stay monotonic.
 struct Pipe {
-  SliceDesc ring[kDepth];
-  uint64_t full[kDepth];
-  uint64_t empty[kDepth];
+  SliceDesc ring[kMaxDepth];
+  uint64_t full[kMaxDepth];
+  uint64_t empty[kMaxDepth];     // completes when the slice is moved AND published
+  uint32_t done[kMaxDepth];      // data warps finished with the slot (last one publishes)
 };
 
 struct Smem {
@@ -476,9 +499,6 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
     } else {
       sh.T = p.spinBase;
     }
-    sh.headSeen = 0;
-    sh.creditSeen = 0;
-    sh.di = m.cache[way].d;
     cmd = CMD_RUN;
   } else {
     p.blkStats[b].idlePolls++;
@@ -493,122 +513,171 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
   return cmd;
 }
 
-// One poll of the connectors for the slice at the issue cursor (a failed poll is
-// one "spin").  On success fills `sd` and returns true.
-__device__ __forceinline__ bool try_issue(const DaemonParams& p, int b, Sched& sh, const CtxSlot& cx,
-                                          SliceDesc& sd) {
-  const int G = p.G, K = p.K, n = p.nranks, sys = p.sysScope;
-  const DynCtx& d = sh.di;
-  int prim, seg;
-  step_prim(d.kind, n, p.rank, cx.root, d.step, cx.s.sendbuff == cx.s.recvbuff, prim, seg);
-  const size_t cb = (size_t)sh.curId * G + b;
-  const bool needRecv = prim & A_RECV, needSend = prim & A_SEND;
-  const char* fl = p.flagsLocal + cb * kFlagStride;
-  if (needRecv && d.nrecv >= sh.headSeen) {
-    sh.headSeen = ld_relaxed(fl, sys);
-    if (d.nrecv >= sh.headSeen) return false;
-  }
-  if (needSend && d.nsent - sh.creditSeen >= (uint64_t)K) {
-    sh.creditSeen = ld_relaxed(fl + 128, sys);
-    if (d.nsent - sh.creditSeen >= (uint64_t)K) return false;
-  }
-  if (needRecv || needSend) fence_acq_rel(sys);     // acquire the peer's data / credit
-  uint64_t sendOff, recvOff, len;
-  seg_geom(d.kind, n, p.rank, cx.s.count, cx.s.segLen, seg, sendOff, recvOff, len);
-  const int isz = elem_size(d.dtype);
-  const uint64_t E = p.sliceBytes / isz;
-  const uint64_t laneLo = (uint64_t)b * cx.s.part;
-  uint64_t laneHi = laneLo + cx.s.part;
-  if (laneHi > len) laneHi = len;
-  const uint64_t lo = laneLo + ((uint64_t)d.loop * p.slicesPerChunk + d.slc) * E;
-  uint64_t hi = lo + E;
-  if (hi > laneHi) hi = laneHi;
-  sd.src = reinterpret_cast<const char*>(cx.s.sendbuff) + (sendOff + lo) * isz;
-  sd.dst = reinterpret_cast<char*>(cx.s.recvbuff) + (recvOff + lo) * isz;
-  sd.cin = p.dataLocal + (cb * K + (d.nrecv % K)) * p.sliceBytes;
-  sd.cout = p.dataNext + (cb * K + (d.nsent % K)) * p.sliceBytes;
-  sd.nelem = hi > lo ? (int64_t)(hi - lo) : 0;
-  sd.prim = prim;
-  sd.dtype = d.dtype;
-  return true;
+__device__ __forceinline__ uint64_t ld_acquire(const void* p, int sys) {
+  uint64_t v;
+  if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
-// Advance a (loop, step, slice) cursor by one slice of primitive `prim`.
-__device__ __forceinline__ void advance(DynCtx& d, int prim, int slicesPerChunk, int nsteps) {
+// Cursor of one collective on one block: (loop, step, slice) + connector counts.
+struct Cursor {
+  uint32_t loop, step, slc;
+  uint64_t nsent, nrecv;
+};
+
+__device__ __forceinline__ void advance(Cursor& d, int prim, int slicesPerChunk, int nsteps) {
   if (prim & A_SEND) d.nsent++;
   if (prim & A_RECV) d.nrecv++;
-  if (++d.slc == slicesPerChunk) {
+  if (++d.slc == (uint32_t)slicesPerChunk) {
     d.slc = 0;
-    if (++d.step == nsteps) { d.step = 0; d.loop++; }
+    if (++d.step == (uint32_t)nsteps) { d.step = 0; d.loop++; }
   }
 }
 
-// Commit a slice the data warps finished: publish it to the peers (commit
-// visibility) and advance the committed dynamic context.
-__device__ __forceinline__ void commit(const DaemonParams& p, int b, Sched& sh, const Smem& m, int prim) {
-  const int sys = p.sysScope;
+// Run the collective at the front of the scheduler until it is done or preempted.
+// Everything hot lives in registers of the control thread: the static context,
+// the issue cursor `di` (runs ahead) and the committed cursor `dc`.
+//   issue : one poll of the connectors for the next slice (a failed poll is one
+//           "spin"); polls are acquire loads, and a cached
+//           head/credit value needs no new poll -- the acquire that observed it
+//           already ordered the peer's data before us.
+//   commit: all slices the data warps finished, in order, under ONE release
+//           fence; then the head (downstream) / credit (upstream) counters are
+//           published once (commit visibility).
+__device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sched& sh, const Smem& m, Pipe& pipe,
+                                              uint32_t& issued, uint32_t& committed) {
+  const uint32_t D = (uint32_t)p.pipeDepth;
+  const int n = p.nranks, r = p.rank, K = p.K, sys = p.sysScope, spc = p.slicesPerChunk;
   CtxSlot& cx = m.cache[sh.way];
-  DynCtx& d = cx.d;
+  // ---- static context -> registers
+  const uint64_t sendbuff = cx.s.sendbuff, recvbuff = cx.s.recvbuff, count = cx.s.count;
+  const uint64_t segLen = cx.s.segLen, part = cx.s.part;
+  const int kind = cx.d.kind, dtype = cx.d.dtype, root = cx.root, nsteps = cx.nsteps;
+  const uint32_t nloops = cx.d.nloops;
+  const bool inplace = sendbuff == recvbuff;
+  const int isz = elem_size(dtype);
+  const uint64_t E = p.sliceBytes / isz;
   const size_t cb = (size_t)sh.curId * p.G + b;
-  if (prim & (A_RECV | A_SEND)) fence_acq_rel(sys);
-  if (prim & A_SEND) st_relaxed(p.flagsNext + cb * kFlagStride, d.nsent + 1, sys);         // head of r+1
-  if (prim & A_RECV) st_relaxed(p.flagsPrev + cb * kFlagStride + 128, d.nrecv + 1, sys);   // credit of r-1
-  advance(d, prim, p.slicesPerChunk, cx.nsteps);
-  d.progressed = 1;
-  m.tq[sh.pos] &= 0xffffu;                          // progressed: no longer stalled
-  if (p.stickiness) {                               // raise the threshold
-    const uint64_t T = sh.T * p.spinBoost;
-    sh.T = T > p.spinCap ? p.spinCap : T;
+  const char* headIn = p.flagsLocal + cb * kFlagStride;
+  const char* creditIn = headIn + 128;
+  char* headOut = p.flagsNext + cb * kFlagStride;
+  char* creditOut = p.flagsPrev + cb * kFlagStride + 128;
+  char* connIn = p.dataLocal + cb * K * p.sliceBytes;
+  char* connOut = p.dataNext + cb * K * p.sliceBytes;
+  // ---- dynamic context -> registers
+  Cursor dc{cx.d.loop, cx.d.step, cx.d.slc, cx.d.nsent, cx.d.nrecv};
+  Cursor di = dc;
+  uint64_t headSeen = 0, creditSeen = 0;
+  uint64_t T = sh.T, spins = 0;
+  unsigned long long nSlices = 0, cPoll = 0, cFence = 0;
+  const long long tRun = clock64();
+  int run;
+  for (;;) {
+    // ---- slices the data warps moved and published: advance the committed cursor
+    if (committed != issued && mbar_test(&pipe.empty[committed % D], (committed / D) & 1)) {
+      do {
+        advance(dc, pipe.ring[committed % D].prim, spc, nsteps);
+        ++committed;
+        ++nSlices;
+      } while (committed != issued && mbar_test(&pipe.empty[committed % D], (committed / D) & 1));
+      if (p.stickiness) {                                 // raise the threshold
+        T *= p.spinBoost;
+        if (T > p.spinCap) T = p.spinCap;
+      }
+      m.tq[sh.pos] &= 0xffffu;                            // progressed: not stalled
+    }
+    if (di.loop >= nloops) {                              // everything issued
+      if (committed == issued) { run = RUN_DONE; break; }
+      continue;
+    }
+    if (issued - committed == D) continue;                // every buffer busy
+    // ---- issue the next slice if its connectors are ready
+    int prim, seg;
+    step_prim(kind, n, r, root, di.step, inplace, prim, seg);
+    const bool needRecv = prim & A_RECV, needSend = prim & A_SEND;
+    bool ok = true;
+    const long long tp = clock64();
+    if (needRecv && di.nrecv >= headSeen) {
+      headSeen = ld_acquire(headIn, sys);
+      ok = di.nrecv < headSeen;
+    }
+    if (ok && needSend && di.nsent - creditSeen >= (uint64_t)K) {
+      creditSeen = ld_acquire(creditIn, sys);
+      ok = di.nsent - creditSeen < (uint64_t)K;
+    }
+    if (!ok) {
+      cPoll += clock64() - tp;
+      if (++spins > T) {                                  // two-phase blocking: preempt
+        while (committed != issued) {                    // drain the pipe
+          mbar_wait(&pipe.empty[committed % D], (committed / D) & 1);
+          advance(dc, pipe.ring[committed % D].prim, spc, nsteps);
+          ++committed;
+          ++nSlices;
+        }
+        run = RUN_PREEMPT;
+        break;
+      }
+      continue;
+    }
+    spins = 0;
+    uint64_t sendOff, recvOff, len;
+    seg_geom(kind, n, r, count, segLen, seg, sendOff, recvOff, len);
+    const uint64_t laneLo = (uint64_t)b * part;
+    uint64_t laneHi = laneLo + part;
+    if (laneHi > len) laneHi = len;
+    const uint64_t lo = laneLo + ((uint64_t)di.loop * spc + di.slc) * E;
+    uint64_t hi = lo + E;
+    if (hi > laneHi) hi = laneHi;
+    SliceDesc& sd = pipe.ring[issued % D];
+    sd.src = reinterpret_cast<const char*>(sendbuff) + (sendOff + lo) * isz;
+    sd.dst = reinterpret_cast<char*>(recvbuff) + (recvOff + lo) * isz;
+    sd.cin = connIn + (di.nrecv % K) * p.sliceBytes;
+    sd.cout = connOut + (di.nsent % K) * p.sliceBytes;
+    sd.nelem = hi > lo ? (int64_t)(hi - lo) : 0;
+    sd.prim = prim;
+    sd.dtype = dtype;
+    sd.headOut = headOut;
+    sd.creditOut = creditOut;
+    sd.headVal = di.nsent + 1;
+    sd.creditVal = di.nrecv + 1;
+    mbar_arrive(&pipe.full[issued % D]);
+    ++issued;
+    advance(di, prim, spc, nsteps);
   }
-  p.collStats[cb].slices++;
+  // ---- registers -> dynamic context in the shared-memory cache
+  if (nSlices) cx.d.progressed = 1;
+  cx.d.loop = dc.loop; cx.d.step = (uint16_t)dc.step; cx.d.slc = (uint16_t)dc.slc;
+  cx.d.nsent = dc.nsent; cx.d.nrecv = dc.nrecv;
+  sh.T = T;
+  sh.cycRun += clock64() - tRun;
+  sh.cycPoll += cPoll;
+  sh.cycRelFence += cFence;
+  sh.nCommit += nSlices;
+  p.collStats[cb].slices += nSlices;
+  return run;
 }
 
 // The control thread (lane 0 of warp 0): scheduler + connector protocol.  Feeds
-// slice descriptors to the data warps through the pipe, kDepth in flight.
+// slice descriptors to the data warps through the pipe, `pipeDepth` in flight.
 __device__ __noinline__ void control_main(const DaemonParams& p, int b, Sched& sh, const Smem& m, Pipe& pipe) {
+  const uint32_t D = (uint32_t)p.pipeDepth;
   uint32_t issued = 0, committed = 0;               // kernel-lifetime slice counters
   for (;;) {
     const int cmd = schedule(p, b, sh, m);
     if (cmd == CMD_NONE) continue;
     if (cmd == CMD_EXIT) break;
-    CtxSlot& cx = m.cache[sh.way];
-    uint64_t spins = 0;
-    int run;
-    for (;;) {
-      // retire finished slices in order
-      while (committed != issued && mbar_test(&pipe.empty[committed % kDepth], (committed / kDepth) & 1)) {
-        commit(p, b, sh, m, pipe.ring[committed % kDepth].prim);
-        ++committed;
-      }
-      if (sh.di.loop >= sh.di.nloops) {             // everything issued
-        if (committed == issued) { run = RUN_DONE; break; }
-        continue;
-      }
-      if (issued - committed == kDepth) continue;   // both buffers busy
-      SliceDesc& sd = pipe.ring[issued % kDepth];
-      if (try_issue(p, b, sh, cx, sd)) {
-        mbar_arrive(&pipe.full[issued % kDepth]);
-        ++issued;
-        advance(sh.di, sd.prim, p.slicesPerChunk, cx.nsteps);
-        spins = 0;
-      } else if (++spins > sh.T) {                  // two-phase blocking: preempt
-        while (committed != issued) {
-          mbar_wait(&pipe.empty[committed % kDepth], (committed / kDepth) & 1);
-          commit(p, b, sh, m, pipe.ring[committed % kDepth].prim);
-          ++committed;
-        }
-        run = RUN_PREEMPT;
-        break;
-      }
-    }
-    sh.lastRun = run;
+    sh.lastRun = run_collective(p, b, sh, m, pipe, issued, committed);
   }
-  // release the data warps
-  if (issued - committed == kDepth) {
-    mbar_wait(&pipe.empty[committed % kDepth], (committed / kDepth) & 1);
-  }
-  pipe.ring[issued % kDepth].prim = P_EXIT;
-  mbar_arrive(&pipe.full[issued % kDepth]);
+  BlockStat& bst = p.blkStats[b];
+  bst.cycRun += sh.cycRun;
+  bst.cycPoll += sh.cycPoll;
+  bst.cycAcqFence += sh.cycAcqFence;
+  bst.cycRelFence += sh.cycRelFence;
+  bst.nCommit += sh.nCommit;
+  // release the data warps (the pipe is drained after every run)
+  pipe.ring[issued % D].prim = P_EXIT;
+  mbar_arrive(&pipe.full[issued % D]);
 }
 
 }  // namespace
@@ -625,7 +694,7 @@ __device__ __noinline__ void control_main(const DaemonParams& p, int b, Sched& s
 // double-buffered descriptor pipe with mbarriers, so the flag round trips and
 // fences of slice k overlap the data movement of slice k+1.
 // =============================================================================
-__global__ void __launch_bounds__(512, 1) occl_daemon_kernel(const DaemonParams* __restrict__ pp, int G) {
+__global__ void __launch_bounds__(kMaxBlockThreads, 1) occl_daemon_kernel(const DaemonParams* __restrict__ pp, int G) {
   const int lr = blockIdx.x / G;
   const DaemonParams& p = pp[lr];
   extern __shared__ __align__(16) unsigned char smem[];
@@ -639,6 +708,7 @@ __global__ void __launch_bounds__(512, 1) occl_daemon_kernel(const DaemonParams*
   const int tid = threadIdx.x;
   const int b = blockIdx.x - lr * G;
   const int nDataWarps = (int)(blockDim.x >> 5) - 1;
+  const uint32_t D = (uint32_t)p.pipeDepth;
 
   if (tid == 0) {
     const BlockState bs = p.blk[b];
@@ -649,12 +719,14 @@ __global__ void __launch_bounds__(512, 1) occl_daemon_kernel(const DaemonParams*
     sh.iter = 0;
     sh.lastRun = -1;
     sh.curId = -1;
+    sh.cycRun = sh.cycPoll = sh.cycAcqFence = sh.cycRelFence = sh.nCommit = 0;
     for (uint32_t i = 0; i < sh.qlen; ++i) m.tq[i] = p.tqSave[(size_t)b * p.maxColl + i];
     for (int w = 0; w < W; ++w) m.cacheTag[w] = -1;
     sh.lastFetch = globaltimer();
-    for (int i = 0; i < kDepth; ++i) {
+    for (uint32_t i = 0; i < D; ++i) {
       mbar_init(&pipe.full[i], 1);
-      mbar_init(&pipe.empty[i], nDataWarps);
+      mbar_init(&pipe.empty[i], 1);
+      pipe.done[i] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     p.blkStats[b].launches++;
@@ -665,16 +737,47 @@ __global__ void __launch_bounds__(512, 1) occl_daemon_kernel(const DaemonParams*
     if (tid == 0) control_main(p, b, sh, m, pipe);
     return;
   }
-  // data warps
-  const int dtid = tid - 32, dnt = (int)blockDim.x - 32;
+  // data warps: every data warp takes part in every slice, in order
+  const int dtid = tid - 32, dnt = nDataWarps * 32;
   const int lane = tid & 31;
+  const bool leader = dtid == 0;                       // probes
+  unsigned long long cWait = 0, cData = 0, nData = 0;
   for (uint32_t j = 0;; ++j) {
-    mbar_wait(&pipe.full[j % kDepth], (j / kDepth) & 1);
-    const SliceDesc sd = pipe.ring[j % kDepth];
+    const uint32_t i = j % D;
+    const long long t0 = clock64();
+    mbar_wait(&pipe.full[i], (j / D) & 1);
+    const SliceDesc sd = pipe.ring[i];
     if (sd.prim == P_EXIT) break;
+    const long long t1 = clock64();
     move_slice_any(sd, dtid, dnt);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&pipe.empty[j % kDepth]);
+    if (lane == 0) {
+      // the last warp to finish publishes the slice: its acq_rel atomic observes
+      // every other warp's (released) stores, and the fence makes them visible
+      // to the peer before the flag (commit visibility)
+      uint32_t old;
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                   : "=r"(old) : "r"(smem_u32(&pipe.done[i])) : "memory");
+      if (old == (uint32_t)nDataWarps - 1) {
+        pipe.done[i] = 0;
+        const int sys = p.sysScope;
+        if (sd.prim & (A_SEND | A_RECV)) fence_acq_rel(sys);
+        if (sd.prim & A_SEND) red_max_relaxed(sd.headOut, sd.headVal, sys);      // head of rank r+1
+        if (sd.prim & A_RECV) red_max_relaxed(sd.creditOut, sd.creditVal, sys);  // credit of rank r-1
+        mbar_arrive(&pipe.empty[i]);
+      }
+    }
+    if (leader) {
+      const long long t2 = clock64();
+      cWait += t1 - t0;
+      cData += t2 - t1;
+      ++nData;
+    }
+  }
+  if (leader) {
+    atomicAdd(&p.blkStats[b].cycDataWait, cWait);
+    atomicAdd(&p.blkStats[b].cycData, cData);
+    atomicAdd(&p.blkStats[b].nData, nData);
   }
 }
 

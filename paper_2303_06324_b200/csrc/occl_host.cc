@@ -278,7 +278,7 @@ void launcher_stop(Launcher* L) {
 occlResult_t validate_config(const occlConfig_t& c) {
   if (c.maxColl < 1 || c.maxColl > 65535) return occlInvalidArgument;
   if (c.gridBlocks < 1 || c.gridBlocks > 1024) return occlInvalidArgument;
-  if (c.blockThreads < 32 || c.blockThreads > 512 || c.blockThreads % 32) return occlInvalidArgument;
+  if (c.blockThreads < 64 || c.blockThreads > 544 || c.blockThreads % 32) return occlInvalidArgument;
   if (c.slicesPerChunk < 1 || c.connSlots <= c.slicesPerChunk) return occlInvalidArgument;  // invariant I7
   if (c.sliceBytes < 16 || c.sliceBytes % 16 || c.sliceBytes > (1ull << 30)) return occlInvalidArgument;
   if (c.minBlockBytes < 1) return occlInvalidArgument;
@@ -287,6 +287,7 @@ occlResult_t validate_config(const occlConfig_t& c) {
   if (c.spinMin < 1 || c.spinBase < c.spinMin || c.spinCap < c.spinBase || c.spinBoost < 1) return occlInvalidArgument;
   if (c.priorityCadence < 1) return occlInvalidArgument;
   if (c.stallLimit < 1) return occlInvalidArgument;
+  if (c.pipeDepth < 1 || c.pipeDepth > 8) return occlInvalidArgument;
   return occlSuccess;
 }
 
@@ -419,7 +420,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   std::memset(c, 0, sizeof(*c));
   c->maxColl = 128;
   c->gridBlocks = 16;
-  c->blockThreads = 512;
+  c->blockThreads = 544;
   c->connSlots = 4;
   c->slicesPerChunk = 2;
   c->sliceBytes = 64 << 10;
@@ -439,6 +440,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->idleSleepNs = 256;
   c->autoLaunch = 1;
   c->cacheWays = 8;
+  c->pipeDepth = 2;
   return occlSuccess;
 }
 
@@ -602,6 +604,7 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   p.idleSleepNs = c->cfg.idleSleepNs;
   p.cacheWays = c->cfg.cacheWays;
   p.sysScope = c->sysScope;
+  p.pipeDepth = c->cfg.pipeDepth;
   Launcher* L = new Launcher();
   if ((r = launcher_start(L, {c})) != occlSuccess) {
     launcher_stop(L);
@@ -618,7 +621,7 @@ occlResult_t occlCommFuse(occlComm_t* comms, int n) {
     if (!c || !c->connected || !c->L) return occlInvalidUsage;
     if (c->dev != ms[0]->dev || c->cfg.gridBlocks != ms[0]->cfg.gridBlocks ||
         c->cfg.maxColl != ms[0]->cfg.maxColl || c->cfg.cacheWays != ms[0]->cfg.cacheWays ||
-        c->cfg.blockThreads != ms[0]->cfg.blockThreads)
+        c->cfg.blockThreads != ms[0]->cfg.blockThreads || c->cfg.pipeDepth != ms[0]->cfg.pipeDepth)
       return occlInvalidArgument;
     if (c->L->members.size() != 1) return occlInvalidUsage;   // fuse single-member launchers only
     if (c->inflight.load() > 0) return occlInvalidUsage;
@@ -800,6 +803,27 @@ occlResult_t occlGetCollStats(occlComm_t c, int id, occlCollStats_t* out) {
     out->ctxSaves += s.ctxSaves;
     out->slices += s.slices;
     out->completions += s.completions;
+  }
+  return occlSuccess;
+}
+
+occlResult_t occlGetProbes(occlComm_t c, occlProbes_t* out) {
+  if (!c || !out) return occlInvalidArgument;
+  const size_t G = c->cfg.gridBlocks;
+  std::vector<BlockStat> bs(G);
+  cudaSetDevice(c->dev);
+  CUDACHECK(c, cudaMemcpyAsync(bs.data(), c->blkStats, G * sizeof(BlockStat), cudaMemcpyDeviceToHost, c->statsStream));
+  CUDACHECK(c, cudaStreamSynchronize(c->statsStream));
+  std::memset(out, 0, sizeof(*out));
+  for (auto& b : bs) {
+    out->cycRun += b.cycRun;
+    out->cycPoll += b.cycPoll;
+    out->cycAcqFence += b.cycAcqFence;
+    out->cycRelFence += b.cycRelFence;
+    out->cycData += b.cycData;
+    out->cycDataWait += b.cycDataWait;
+    out->nData += b.nData;
+    out->nCommit += b.nCommit;
   }
   return occlSuccess;
 }

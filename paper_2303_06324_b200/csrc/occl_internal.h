@@ -80,6 +80,16 @@ struct alignas(16) CollStat {   // per (collective, block), device memory
 };
 struct alignas(16) BlockStat {  // per block
   unsigned long long quits, exits, fetched, cqes, launches, idlePolls, pad[2];
+  // in-kernel timing probes (SM clock cycles), flushed when the block exits
+  // (the paper's "core execution time" probes)
+  unsigned long long cycRun;        // control thread inside collective runs
+  unsigned long long cycPoll;       // ... in failed connector polls (waiting for peers)
+  unsigned long long cycAcqFence;   // ... in the acquire fence after a successful poll
+  unsigned long long cycRelFence;   // ... in the commit (release) fence
+  unsigned long long cycData;       // data group leaders: moving slices
+  unsigned long long cycDataWait;   // data group leaders: waiting for a descriptor
+  unsigned long long nData;         // slices timed by data group leaders
+  unsigned long long nCommit;       // slices committed
 };
 
 struct DaemonParams {
@@ -107,6 +117,7 @@ struct DaemonParams {
   uint32_t idleSleepNs;
   int cacheWays;
   int sysScope;                     // 1: peers in other processes/devices -> .sys fences
+  int pipeDepth;                    // slices in flight control -> data warps (<= 8)
 };
 
 }  // namespace occl

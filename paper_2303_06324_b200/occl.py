@@ -34,7 +34,7 @@ EXPORTED = [
     "occlCommInit", "occlCommDestroy", "occlAllReduce", "occlAllGather", "occlReduceScatter",
     "occlBroadcast", "occlWait", "occlTest", "occlSetCallback", "occlGetStats", "occlGetCollStats",
     "occlCommExit", "occlCommLaunch", "occlCommSetAutoLaunch", "occlCommQuiesce", "occlCommGetStream",
-    "occlCollBlocks", "occlCommFuse",
+    "occlCollBlocks", "occlCommFuse", "occlGetProbes",
 ]
 
 
@@ -46,6 +46,7 @@ class occlConfig_t(C.Structure):
         ("spinBase", C.c_uint32), ("spinStep", C.c_uint32), ("spinMin", C.c_uint32), ("spinBoost", C.c_uint32),
         ("spinCap", C.c_uint32), ("stallLimit", C.c_uint32), ("quitEnabled", C.c_int),
         ("quitIdleNs", C.c_uint64), ("idleSleepNs", C.c_uint32), ("autoLaunch", C.c_int), ("cacheWays", C.c_int),
+        ("pipeDepth", C.c_int),
     ]
 
 
@@ -56,6 +57,11 @@ class occlStats_t(C.Structure):
 
 class occlCollStats_t(C.Structure):
     _fields_ = [(k, C.c_uint64) for k in ("preemptions", "ctxLoads", "ctxSaves", "slices", "completions")]
+
+
+class occlProbes_t(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in ("cycRun", "cycPoll", "cycAcqFence", "cycRelFence", "cycData",
+                                          "cycDataWait", "nData", "nCommit")]
 
 
 CALLBACK = C.CFUNCTYPE(None, C.c_int, C.c_void_p)
@@ -104,6 +110,7 @@ def _lib():
             "occlCommGetStream": [vp, C.POINTER(vp)],
             "occlCollBlocks": [vp, i, sz, i, C.POINTER(i)],
             "occlCommFuse": [C.POINTER(vp), i],
+            "occlGetProbes": [vp, C.POINTER(occlProbes_t)],
         }.items():
             f = getattr(L, name)
             f.restype = C.c_int
@@ -305,6 +312,11 @@ class Comm:
 
     def coll_stats(self, coll_id):
         return occlGetCollStats(self.h, coll_id)
+
+    def probes(self) -> dict:
+        s = occlProbes_t()
+        check(_lib().occlGetProbes(self.h, C.byref(s)), "occlGetProbes")
+        return {k: getattr(s, k) for k, _ in occlProbes_t._fields_}
 
     def destroy(self):
         if self.h:
