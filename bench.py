@@ -46,12 +46,13 @@ def parse():
     ap.add_argument("--size-mib", type=float, default=256.0)
     ap.add_argument("--ranks", type=int, default=8)
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "i32"])
-    ap.add_argument("--grid-blocks", type=int, default=16)
+    ap.add_argument("--grid-blocks", type=int, default=18)
     ap.add_argument("--slice-kib", type=int, default=64)
     ap.add_argument("--conn-slots", type=int, default=4)
     ap.add_argument("--slices-per-chunk", type=int, default=2)
-    ap.add_argument("--threads", type=int, default=544)
-    ap.add_argument("--pipe-depth", type=int, default=2)
+    ap.add_argument("--threads", type=int, default=576)
+    ap.add_argument("--pipe-depth", type=int, default=4)
+    ap.add_argument("--prefetch", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--check", action="store_true", help="sampled oracle check of the timed output")
@@ -200,6 +201,7 @@ def make_ring(args, world, prank, dev, dist):
     cfg = occl.occlConfigDefault(gridBlocks=args.grid_blocks, sliceBytes=args.slice_kib * 1024,
                                  connSlots=args.conn_slots, slicesPerChunk=args.slices_per_chunk,
                                  blockThreads=args.threads, pipeDepth=args.pipe_depth,
+                                 prefetchSlices=args.prefetch,
                                  maxColl=128, autoLaunch=0)
     hs = [occl.occlCommCreate(R, prank * V + i, dev, cfg) for i in range(V)]
     mine = [occl.occlCommGetHandle(h) for h in hs]
@@ -399,7 +401,7 @@ def run_occl(args):
                    "ranks": R, "ranks_per_gpu": V, "size_bytes_per_rank": size, "grid_blocks": args.grid_blocks,
                    "slice_bytes": args.slice_kib * 1024, "conn_slots": args.conn_slots,
                    "slices_per_chunk": args.slices_per_chunk, "block_threads": args.threads,
-                   "pipe_depth": args.pipe_depth, "l2": "inputs larger than L2 (R x S >> 126 MB)",
+                   "pipe_depth": args.pipe_depth, "prefetch_slices": args.prefetch, "l2": "inputs larger than L2 (R x S >> 126 MB)",
                    "algbw_GBps": size / (ms_step / 1e3) / 1e9},
         "gpu_launches": launches,
         "clocks": clk.summary(),

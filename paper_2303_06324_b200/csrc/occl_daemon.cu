@@ -312,7 +312,9 @@ enum : int { CMD_NONE = 0, CMD_RUN = 1, CMD_EXIT = 2 };
 enum : int { RUN_PREEMPT = 0, RUN_GO = 1, RUN_DONE = 2 };
 constexpr int P_EXIT = 0x100;          // descriptor telling the data warps to leave
 constexpr int kMaxDepth = 8;           // max slices in flight between control and data warps
-constexpr int kMaxBlockThreads = 544;  // 1 control warp + up to 16 data warps
+constexpr int kMaxBlockThreads = 576;  // control warp + TMA producer warp + up to 16 compute warps
+constexpr int kTile = 16384;           // TMA staging tile (bytes per operand)
+constexpr int kStages = 6;             // staging ring depth: up to 6 x 2 x 16 KiB of loads in flight
 
 // Scheduler state of one block; touched only by the control thread.
 struct Sched {
@@ -568,6 +570,9 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   // ---- dynamic context -> registers
   Cursor dc{cx.d.loop, cx.d.step, cx.d.slc, cx.d.nsent, cx.d.nrecv};
   Cursor di = dc;
+  Cursor dpf = dc;                                        // L2 prefetch cursor (runs ahead of di)
+  uint32_t pfAhead = 0;
+  const uint64_t laneLo = (uint64_t)b * part;
   uint64_t headSeen = 0, creditSeen = 0;
   uint64_t T = sh.T, spins = 0;
   unsigned long long nSlices = 0, cPoll = 0, cFence = 0;
@@ -623,7 +628,6 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     spins = 0;
     uint64_t sendOff, recvOff, len;
     seg_geom(kind, n, r, count, segLen, seg, sendOff, recvOff, len);
-    const uint64_t laneLo = (uint64_t)b * part;
     uint64_t laneHi = laneLo + part;
     if (laneHi > len) laneHi = len;
     const uint64_t lo = laneLo + ((uint64_t)di.loop * spc + di.slc) * E;
@@ -644,6 +648,35 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     mbar_arrive(&pipe.full[issued % D]);
     ++issued;
     advance(di, prim, spc, nsteps);
+    if (pfAhead) --pfAhead;
+    // ---- prefetch the send-buffer operand of the slices ahead into L2 (TMA
+    // prefetch): it has no peer dependency, so the loads on the critical path
+    // of the ring hop hit L2 instead of DRAM
+    while (pfAhead < (uint32_t)p.prefetchSlices && dpf.loop < nloops) {
+      if (dpf.loop < di.loop || (dpf.loop == di.loop && (dpf.step < di.step ||
+                                                         (dpf.step == di.step && dpf.slc < di.slc)))) {
+        dpf = di;                                         // never prefetch behind the issue cursor
+      }
+      int pprim, pseg;
+      step_prim(kind, n, r, root, dpf.step, inplace, pprim, pseg);
+      if ((pprim & A_REDUCE) || !(pprim & A_RECV)) {      // primitive reads the send buffer
+        uint64_t so, ro, ln;
+        seg_geom(kind, n, r, count, segLen, pseg, so, ro, ln);
+        uint64_t lh = laneLo + part;
+        if (lh > ln) lh = ln;
+        const uint64_t plo = laneLo + ((uint64_t)dpf.loop * spc + dpf.slc) * E;
+        uint64_t phi = plo + E;
+        if (phi > lh) phi = lh;
+        if (phi > plo) {
+          const char* a = reinterpret_cast<const char*>(sendbuff) + (so + plo) * isz;
+          const uint64_t bytes = ((phi - plo) * isz) & ~(uint64_t)15;
+          if (bytes && !((uintptr_t)a & 15))
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a), "r"((uint32_t)bytes) : "memory");
+        }
+      }
+      advance(dpf, pprim, spc, nsteps);
+      ++pfAhead;
+    }
   }
   // ---- registers -> dynamic context in the shared-memory cache
   if (nSlices) cx.d.progressed = 1;
@@ -680,6 +713,82 @@ __device__ __noinline__ void control_main(const DaemonParams& p, int b, Sched& s
   mbar_arrive(&pipe.full[issued % D]);
 }
 
+// ------------------------------------------------------------------ TMA staging
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;"
+               :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// 1-D bulk copy global -> shared through the TMA unit; completes on `bar`.
+__device__ __forceinline__ void tma_load(void* smemDst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_u32(smemDst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ uint4 lds_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
+
+// A slice goes through the TMA staging ring when its vector part is 16-B aligned
+// (connector slots always are; user buffers almost always).  Otherwise the
+// compute warps move it with register loads (move_slice).
+__device__ __forceinline__ int tma_vec_bytes(const SliceDesc& d) {
+  const int isz = d.dtype == kBF16 ? 2 : 4;
+  if (d.nelem <= 0) return 0;
+  if ((((uintptr_t)d.src) | ((uintptr_t)d.dst)) & 15) return 0;
+  return (int)((d.nelem * isz) & ~(int64_t)15);
+}
+
+struct Stage {                 // one staging slot: the incoming operand and the local operand
+  uint4 in[kTile / 16];
+  uint4 loc[kTile / 16];
+};
+
+// Producer lane (warp 1 lane 0): streams every slice's operands into the staging
+// ring with cp.async.bulk, kStages tiles ahead of the compute warps.
+__device__ __noinline__ void producer_main(const DaemonParams& p, Pipe& pipe, Stage* st, uint64_t* tfull,
+                                           uint64_t* tempty) {
+  const uint32_t D = (uint32_t)p.pipeDepth;
+  uint32_t c = 0;
+  for (uint32_t j = 0;; ++j) {
+    mbar_wait(&pipe.full[j % D], (j / D) & 1);
+    const SliceDesc sd = pipe.ring[j % D];
+    if (sd.prim == P_EXIT) break;
+    const int vb = tma_vec_bytes(sd);
+    if (vb == 0) continue;
+    // order the acquire of the peer's head (generic proxy) before the bulk reads (async proxy)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    const bool recv = sd.prim & A_RECV, reduce = sd.prim & A_REDUCE;
+    const char* in = recv ? sd.cin : sd.src;
+    for (int off = 0; off < vb; off += kTile, ++c) {
+      const uint32_t s = c % kStages, u = c / kStages;
+      mbar_wait(&tempty[s], (u & 1) ^ 1);
+      const uint32_t sz = (uint32_t)min(kTile, vb - off);
+      mbar_expect_tx(&tfull[s], reduce ? 2 * sz : sz);
+      tma_load(st[s].in, in + off, sz, &tfull[s]);
+      if (reduce) tma_load(st[s].loc, sd.src + off, sz, &tfull[s]);
+    }
+  }
+}
+
+// Compute warps: reduce / copy the staged tiles into the recv buffer and the
+// downstream connector with 128-bit stores.
+template <int DT>
+__device__ __forceinline__ void consume_tile(const SliceDesc& d, const Stage& s, int off, int sz, int tid, int nt) {
+  const int prim = d.prim;
+  const bool reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
+  uint4* vd = reinterpret_cast<uint4*>(d.dst + off);
+  uint4* vo = reinterpret_cast<uint4*>(d.cout + off);
+  const int nv = sz >> 4;
+  for (int i = tid; i < nv; i += nt) {
+    uint4 v = lds_v4(&s.in[i]);
+    if (reduce) v = vadd<DT>(v, lds_v4(&s.loc[i]));
+    if (copy) __stcg(vd + i, v);
+    if (send) __stcg(vo + i, v);
+  }
+}
+
 }  // namespace
 
 // =============================================================================
@@ -690,24 +799,28 @@ __device__ __noinline__ void control_main(const DaemonParams& p, int b, Sched& s
 // connectors -- the per-rank daemons are then co-resident by construction.
 //
 // Warp roles: warp 0 lane 0 is the control thread (scheduler, SQ/CQ, connector
-// flags, context switches); warps 1.. move data.  They communicate through a
-// double-buffered descriptor pipe with mbarriers, so the flag round trips and
-// fences of slice k overlap the data movement of slice k+1.
+// flags, context switches); warp 1 lane 0 is the TMA producer streaming slice
+// operands into a shared-memory staging ring (cp.async.bulk); warps 2.. are
+// compute warps that reduce/copy staged tiles and store them.  Control and the
+// data warps communicate through a descriptor pipe with mbarriers; the last
+// compute warp to finish a slice publishes it to the peers.
 // =============================================================================
 __global__ void __launch_bounds__(kMaxBlockThreads, 1) occl_daemon_kernel(const DaemonParams* __restrict__ pp, int G) {
   const int lr = blockIdx.x / G;
   const DaemonParams& p = pp[lr];
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Sched sh;
   __shared__ Pipe pipe;
+  __shared__ uint64_t tfull[kStages], tempty[kStages];
   const int W = p.cacheWays;
+  Stage* stages = reinterpret_cast<Stage*>(smem);                       // 128-B aligned
   Smem m;
-  m.cache = reinterpret_cast<CtxSlot*>(smem);
+  m.cache = reinterpret_cast<CtxSlot*>(smem + kStages * sizeof(Stage));
   m.cacheTag = reinterpret_cast<int*>(m.cache + W);
   m.tq = reinterpret_cast<uint32_t*>(m.cacheTag + W);
   const int tid = threadIdx.x;
   const int b = blockIdx.x - lr * G;
-  const int nDataWarps = (int)(blockDim.x >> 5) - 1;
+  const int nComputeWarps = (int)(blockDim.x >> 5) - 2;
   const uint32_t D = (uint32_t)p.pipeDepth;
 
   if (tid == 0) {
@@ -728,20 +841,26 @@ __global__ void __launch_bounds__(kMaxBlockThreads, 1) occl_daemon_kernel(const 
       mbar_init(&pipe.empty[i], 1);
       pipe.done[i] = 0;
     }
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], nComputeWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     p.blkStats[b].launches++;
   }
   __syncthreads();
 
-  if (tid < 32) {
+  if (tid < 64) {
     if (tid == 0) control_main(p, b, sh, m, pipe);
+    else if (tid == 32) producer_main(p, pipe, stages, tfull, tempty);
     return;
   }
-  // data warps: every data warp takes part in every slice, in order
-  const int dtid = tid - 32, dnt = nDataWarps * 32;
+  // compute warps: every compute warp takes part in every slice, in order
+  const int ctid = tid - 64, cnt = nComputeWarps * 32;
   const int lane = tid & 31;
-  const bool leader = dtid == 0;                       // probes
+  const bool leader = ctid == 0;                       // probes
   unsigned long long cWait = 0, cData = 0, nData = 0;
+  uint32_t c = 0;                                      // staged tiles consumed
   for (uint32_t j = 0;; ++j) {
     const uint32_t i = j % D;
     const long long t0 = clock64();
@@ -749,16 +868,54 @@ __global__ void __launch_bounds__(kMaxBlockThreads, 1) occl_daemon_kernel(const 
     const SliceDesc sd = pipe.ring[i];
     if (sd.prim == P_EXIT) break;
     const long long t1 = clock64();
-    move_slice_any(sd, dtid, dnt);
+    const int vb = tma_vec_bytes(sd);
+    if (vb == 0) {
+      move_slice_any(sd, ctid, cnt);                   // misaligned: register path
+    } else {
+      for (int off = 0; off < vb; off += kTile, ++c) {
+        const uint32_t s = c % kStages, u = c / kStages;
+        mbar_wait(&tfull[s], u & 1);
+        const int sz = min(kTile, vb - off);
+        if (sd.prim & A_REDUCE) {
+          if (sd.dtype == kF32) consume_tile<kF32>(sd, stages[s], off, sz, ctid, cnt);
+          else if (sd.dtype == kBF16) consume_tile<kBF16>(sd, stages[s], off, sz, ctid, cnt);
+          else consume_tile<kI32>(sd, stages[s], off, sz, ctid, cnt);
+        } else {
+          consume_tile<kI32>(sd, stages[s], off, sz, ctid, cnt);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[s]);
+      }
+      // ragged tail (< 16 B) straight from global memory
+      const int isz = sd.dtype == kBF16 ? 2 : 4;
+      const int64_t e0 = vb / isz;
+      for (int64_t e = e0 + ctid; e < sd.nelem; e += cnt) {
+        const bool rv = sd.prim & A_RECV, rd = sd.prim & A_REDUCE;
+        if (isz == 2) {
+          uint16_t v = __ldcg(reinterpret_cast<const uint16_t*>(rv ? sd.cin : sd.src) + e);
+          if (rd) v = sadd<kBF16>(v, __ldcg(reinterpret_cast<const uint16_t*>(sd.src) + e));
+          if (sd.prim & A_COPY) reinterpret_cast<uint16_t*>(sd.dst)[e] = v;
+          if (sd.prim & A_SEND) reinterpret_cast<uint16_t*>(sd.cout)[e] = v;
+        } else {
+          uint32_t v = __ldcg(reinterpret_cast<const uint32_t*>(rv ? sd.cin : sd.src) + e);
+          if (rd) {
+            const uint32_t w = __ldcg(reinterpret_cast<const uint32_t*>(sd.src) + e);
+            v = sd.dtype == kF32 ? __float_as_uint(__fadd_rn(__uint_as_float(v), __uint_as_float(w))) : v + w;
+          }
+          if (sd.prim & A_COPY) reinterpret_cast<uint32_t*>(sd.dst)[e] = v;
+          if (sd.prim & A_SEND) reinterpret_cast<uint32_t*>(sd.cout)[e] = v;
+        }
+      }
+    }
     __syncwarp();
     if (lane == 0) {
-      // the last warp to finish publishes the slice: its acq_rel atomic observes
-      // every other warp's (released) stores, and the fence makes them visible
-      // to the peer before the flag (commit visibility)
+      // the last compute warp to finish publishes the slice: its acq_rel atomic
+      // observes every other warp's (released) stores, and the fence makes them
+      // visible to the peer before the flag (commit visibility)
       uint32_t old;
       asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
                    : "=r"(old) : "r"(smem_u32(&pipe.done[i])) : "memory");
-      if (old == (uint32_t)nDataWarps - 1) {
+      if (old == (uint32_t)nComputeWarps - 1) {
         pipe.done[i] = 0;
         const int sys = p.sysScope;
         if (sd.prim & (A_SEND | A_RECV)) fence_acq_rel(sys);
@@ -782,7 +939,8 @@ __global__ void __launch_bounds__(kMaxBlockThreads, 1) occl_daemon_kernel(const 
 }
 
 extern "C" size_t occl_internal_daemon_smem(int maxColl, int cacheWays) {
-  return (size_t)cacheWays * sizeof(CtxSlot) + (size_t)cacheWays * sizeof(int) + (size_t)(maxColl + 1) * 4 + 16;
+  return (size_t)kStages * sizeof(Stage) + (size_t)cacheWays * sizeof(CtxSlot) + (size_t)cacheWays * sizeof(int) +
+         (size_t)(maxColl + 1) * 4 + 16;
 }
 
 // `pDev` points to a device-memory array of `nranks` parameter blocks (one per

@@ -278,7 +278,7 @@ void launcher_stop(Launcher* L) {
 occlResult_t validate_config(const occlConfig_t& c) {
   if (c.maxColl < 1 || c.maxColl > 65535) return occlInvalidArgument;
   if (c.gridBlocks < 1 || c.gridBlocks > 1024) return occlInvalidArgument;
-  if (c.blockThreads < 64 || c.blockThreads > 544 || c.blockThreads % 32) return occlInvalidArgument;
+  if (c.blockThreads < 96 || c.blockThreads > 576 || c.blockThreads % 32) return occlInvalidArgument;
   if (c.slicesPerChunk < 1 || c.connSlots <= c.slicesPerChunk) return occlInvalidArgument;  // invariant I7
   if (c.sliceBytes < 16 || c.sliceBytes % 16 || c.sliceBytes > (1ull << 30)) return occlInvalidArgument;
   if (c.minBlockBytes < 1) return occlInvalidArgument;
@@ -288,6 +288,7 @@ occlResult_t validate_config(const occlConfig_t& c) {
   if (c.priorityCadence < 1) return occlInvalidArgument;
   if (c.stallLimit < 1) return occlInvalidArgument;
   if (c.pipeDepth < 1 || c.pipeDepth > 8) return occlInvalidArgument;
+  if (c.prefetchSlices < 0 || c.prefetchSlices > 64) return occlInvalidArgument;
   return occlSuccess;
 }
 
@@ -420,7 +421,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   std::memset(c, 0, sizeof(*c));
   c->maxColl = 128;
   c->gridBlocks = 16;
-  c->blockThreads = 544;
+  c->blockThreads = 576;
   c->connSlots = 4;
   c->slicesPerChunk = 2;
   c->sliceBytes = 64 << 10;
@@ -440,7 +441,8 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->idleSleepNs = 256;
   c->autoLaunch = 1;
   c->cacheWays = 8;
-  c->pipeDepth = 2;
+  c->pipeDepth = 4;
+  c->prefetchSlices = 0;
   return occlSuccess;
 }
 
@@ -605,6 +607,7 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   p.cacheWays = c->cfg.cacheWays;
   p.sysScope = c->sysScope;
   p.pipeDepth = c->cfg.pipeDepth;
+  p.prefetchSlices = c->cfg.prefetchSlices;
   Launcher* L = new Launcher();
   if ((r = launcher_start(L, {c})) != occlSuccess) {
     launcher_stop(L);

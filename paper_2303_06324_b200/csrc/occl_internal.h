@@ -118,6 +118,7 @@ struct DaemonParams {
   int cacheWays;
   int sysScope;                     // 1: peers in other processes/devices -> .sys fences
   int pipeDepth;                    // slices in flight control -> data warps (<= 8)
+  int prefetchSlices;               // L2 prefetch distance for the send-buffer operand (slices)
 };
 
 }  // namespace occl

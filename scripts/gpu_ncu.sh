@@ -1,0 +1,6 @@
+# ncu: launch list + one full capture of the daemon kernel (bench config)
+set -x
+mkdir -p gpurun_out
+ARGS="${BENCH_ARGS:-}"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu $ARGS > gpurun_out/ncu_launch.log 2>&1; echo "ncu1 rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:occl_daemon -c 1 -o gpurun_out/prof_daemon -f python bench.py --steps 2 --warmup 0 --no-e2e --no-cpu $ARGS > gpurun_out/ncu_full.log 2>&1; echo "ncu2 rc=$?"; tail -3 gpurun_out/ncu_full.log

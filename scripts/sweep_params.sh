@@ -1,13 +1,13 @@
 # bench parameter sweep (no e2e / cpu legs); configs from $SWEEP (one per line) or defaults
 mkdir -p gpurun_out
 CFGS="${SWEEP:-
---pipe-depth 2
---pipe-depth 4
---pipe-depth 2 --grid-blocks 18
---pipe-depth 4 --conn-slots 8
---pipe-depth 4 --conn-slots 8 --slice-kib 128
---pipe-depth 2 --slice-kib 32 --conn-slots 8 --slices-per-chunk 4
---pipe-depth 4 --threads 288}"
+--grid-blocks 18
+--grid-blocks 16
+--grid-blocks 18 --pipe-depth 4
+--grid-blocks 18 --slice-kib 128 --conn-slots 4
+--grid-blocks 18 --slice-kib 32 --conn-slots 8 --slices-per-chunk 4
+--grid-blocks 18 --conn-slots 8 --slices-per-chunk 4
+--grid-blocks 18 --threads 320}"
 echo "$CFGS" | while read -r cfg; do
   [ -z "$cfg" ] && continue
   echo "== $cfg"
