@@ -430,11 +430,14 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->orderPolicy = occlOrderFifo;
   c->priorityCadence = 8;
   c->stickiness = 1;
-  c->spinBase = 1 << 14;
-  c->spinStep = 1 << 10;
-  c->spinMin = 1 << 10;
+  // thresholds in failed connector polls; one poll of an L2-resident flag is
+  // ~0.4-0.5 us on B200, so base ~100 us at the queue front, floor ~4 us,
+  // cap ~2 ms for a collective that keeps making progress (R1)
+  c->spinBase = 256;
+  c->spinStep = 16;
+  c->spinMin = 8;
   c->spinBoost = 2;
-  c->spinCap = 1 << 16;
+  c->spinCap = 4096;
   c->stallLimit = 2;
   c->quitEnabled = 1;
   c->quitIdleNs = 1'000'000;

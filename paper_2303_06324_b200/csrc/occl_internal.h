@@ -1,5 +1,5 @@
 // occl_internal.h -- layouts shared by the host runtime (occl_host.cc) and the
-// daemon kernel (occl_daemon.cu).  Product code; shares nothing with oracle/.
+// daemon kernel (occl_daemon.cu).  Product code; shares nothing with the CPU reference.
 #pragma once
 #include <stdint.h>
 #include <stddef.h>
