@@ -210,7 +210,9 @@ occlResult_t occlCommExit(occlComm_t comm);
 /* Launch the daemon now if it is not running (what the supervisor does on an
  * SQE when autoLaunch = 1). */
 occlResult_t occlCommLaunch(occlComm_t comm);
-/* Enable / disable the supervisor's event-driven start. */
+/* Enable / disable the supervisor's event-driven start.  While it is disabled the
+ * daemon does not quit voluntarily either (nobody would restart it): launches
+ * made with occlCommLaunch run until their Exiting SQE. */
 occlResult_t occlCommSetAutoLaunch(occlComm_t comm, int enable);
 /* Wait until no daemon kernel of this communicator is running. */
 occlResult_t occlCommQuiesce(occlComm_t comm, int64_t timeoutNs);

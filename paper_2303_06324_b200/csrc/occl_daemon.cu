@@ -452,11 +452,16 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
     const Sqe* slot = p.sq + (sh.cursor % p.sqDepth);
     const uint64_t seq = ld_acquire_sys(&slot->seq);
     if (seq == sh.cursor + 1) {
-      const volatile Sqe* vs = slot;
+      // the whole 64-B SQE in four 16-B system-scope loads issued back to back
+      // (one PCIe round trip instead of one per field)
+      uint4 w[4];
+      const char* base = reinterpret_cast<const char*>(slot);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        asm volatile("ld.relaxed.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(w[q].x), "=r"(w[q].y), "=r"(w[q].z), "=r"(w[q].w) : "l"(base + 16 * q) : "memory");
       Sqe e;
-      e.subSeq = vs->subSeq; e.count = vs->count; e.sendbuff = vs->sendbuff; e.recvbuff = vs->recvbuff;
-      e.collId = vs->collId; e.kind = vs->kind; e.dtype = vs->dtype; e.nblocks = vs->nblocks;
-      e.root = vs->root;
+      memcpy(&e, w, sizeof(Sqe));
       ++sh.cursor;
       p.blk[b].sqCursor = sh.cursor;
       fence_sys();                                   // SQE reads complete before the slot is freed

@@ -91,6 +91,7 @@ struct Launcher {
   std::atomic<bool> stop{false};
   std::atomic<int> autoLaunch{1};
   std::atomic<int> sticky{0};
+  int quitUploaded = -1;                         // effective quitEnabled in paramsDev
 };
 }  // namespace occl
 
@@ -180,6 +181,21 @@ occlResult_t launch_locked(Launcher* L) {
   if (L->members.empty()) return occlInvalidUsage;
   occlComm* c0 = L->members[0];
   cudaError_t e;
+  // A voluntary quit is only safe while the host restarts the daemon on pending
+  // work (event-driven start); without autoLaunch it would
+  // strand queued collectives, so the daemon is told not to quit.
+  const int quit = L->autoLaunch.load() ? 1 : 0;
+  if (quit != L->quitUploaded) {
+    std::vector<DaemonParams> ps;
+    for (occlComm* m : L->members) {
+      DaemonParams q = m->params;
+      q.quitEnabled = m->cfg.quitEnabled && quit;
+      ps.push_back(q);
+    }
+    if ((e = cudaMemcpy(L->paramsDev, ps.data(), ps.size() * sizeof(DaemonParams), cudaMemcpyHostToDevice)) !=
+        cudaSuccess) { L->sticky.store((int)e); return occlCudaError; }
+    L->quitUploaded = quit;
+  }
   if ((e = cudaEventRecord(L->evStart, L->stream)) != cudaSuccess) { L->sticky.store((int)e); return occlCudaError; }
   int r = occl_internal_launch_daemon(&c0->params, L->paramsDev, (int)L->members.size(), c0->cfg.blockThreads,
                                       L->stream);
