@@ -81,7 +81,7 @@ typedef struct {
   size_t sliceBytes;      /* bytes per connector slot (multiple of 16)                             */
   size_t minBlockBytes;   /* a collective uses ceil(segmentBytes / minBlockBytes) blocks (<= G)   */
   int sqDepth;            /* SQ ring entries                                                       */
-  int orderPolicy;        /* occlOrderFifo | occlOrderPriority                  */
+  int orderPolicy;        /* occlOrderFifo | occlOrderPriority (queue sorted by priority)       */
   int priorityCadence;    /* priority policy: poll the SQ every N scheduling rounds                */
   int stickiness;         /* 1 = paper's spin-threshold policy; 0 = constant    */
   uint32_t spinBase;      /* initial threshold (failed connector polls) at queue position 0       */
@@ -197,6 +197,12 @@ occlResult_t occlTest(occlComm_t comm, int collId, int* done);
 /* Bind a callback fired exactly once per completion of collId by the host
  * poller.  cb == NULL unbinds. */
 occlResult_t occlSetCallback(occlComm_t comm, int collId, occlCallback_t cb, void* arg);
+
+/* User-defined priority of collId for the priority order policy:
+ * lower values run first; the task queues are kept sorted by it.  Like collId it
+ * must be globally agreed.  Default: priority = collId.  Takes effect at the
+ * next submission of collId. */
+occlResult_t occlSetPriority(occlComm_t comm, int collId, int32_t priority);
 
 /* Counters (a snapshot; the daemon may be running). */
 occlResult_t occlGetStats(occlComm_t comm, occlStats_t* out);

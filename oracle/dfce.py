@@ -91,6 +91,7 @@ class CollMeta:
     root: int = 0
     nblocks: int = 1
     inplace: bool = False
+    priority: int | None = None    # priority policy: globally agreed, lower first (default coll_id)
 
 
 @dataclass
@@ -403,9 +404,17 @@ class Simulator:
             del L.cache[way]
         self.queue_len_at_fetch[r].append(len(L.queue))
         if self.cfg.order_policy == "priority" and not self.cfg.baseline:
-            L.queue.insert(0, m.coll_id)
-            if len(L.queue) > 1:
-                L.pos = (L.pos + 1) % len(L.queue)   # keep pointing at the same entry
+            # priority-based ordering, reading R10: the
+            # queue is kept sorted by the user-defined priority (ties: arrival) and
+            # the traversal restarts at the front
+            prio = lambda cid: R.static[(cid, b)].meta.priority if R.static[(cid, b)].meta.priority is not None \
+                else cid
+            at = len(L.queue)
+            while at > 0 and prio(L.queue[at - 1]) > prio(m.coll_id):
+                at -= 1
+            L.queue.insert(at, m.coll_id)
+            L.pos = 0
+            L.T = None
         else:
             L.queue.append(m.coll_id)
         L.stall[m.coll_id] = 0

@@ -342,6 +342,7 @@ struct Smem {
   CtxSlot* cache;      // [W]  direct-mapped context cache
   int* cacheTag;       // [W]
   uint32_t* tq;        // [maxColl] task queue: id | stall << 16
+  int32_t* prio;       // [maxColl] priority of each queued collective (by id)
 };
 
 __device__ __forceinline__ void save_dyn(CtxSlot* g, const DynCtx& d) {
@@ -380,19 +381,29 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, Sched& sh, cons
   ns->d.loop = 0; ns->d.step = 0; ns->d.slc = 0; ns->d.nloops = (uint32_t)nloops;
   ns->d.kind = e.kind; ns->d.dtype = (uint8_t)e.dtype; ns->d.progressed = 0;
   ns->d.nsent = nsent; ns->d.nrecv = nrecv;
-  ns->root = e.root; ns->nblocks = e.nblocks; ns->nsteps = (uint16_t)nsteps;
+  ns->root = e.root; ns->nblocks = e.nblocks; ns->nsteps = (uint16_t)nsteps; ns->priority = e.priority;
   uint4* dst = reinterpret_cast<uint4*>(g);
 #pragma unroll
   for (int i = 0; i < kCtxBytes / 16; ++i) st_cg_v4(dst + i, w[i]);
   const int way = c % W;
   if (m.cacheTag[way] == c) m.cacheTag[way] = -1;
+  m.prio[c] = e.priority;
   if (p.orderPolicy == 0) {
     m.tq[sh.qlen++] = (uint32_t)c;                  // FIFO: tail
   } else {
-    for (uint32_t i = sh.qlen; i > 0; --i) m.tq[i] = m.tq[i - 1];
-    m.tq[0] = (uint32_t)c;                          // priority: front
+    // priority order: the queue is kept sorted by the
+    // user-defined priority (ties: arrival); a collective that outranks the
+    // current front goes to the front and the traversal restarts there.  With a
+    // globally agreed priority every rank's queue has the same order, so the
+    // ranks converge on the same front (de-facto gang scheduling).
+    uint32_t at = sh.qlen;
+    while (at > 0 && m.prio[m.tq[at - 1] & 0xffffu] > e.priority) {
+      m.tq[at] = m.tq[at - 1];
+      --at;
+    }
+    m.tq[at] = (uint32_t)c;
     ++sh.qlen;
-    if (sh.qlen > 1) sh.pos = (sh.pos + 1) % sh.qlen;
+    sh.pos = 0;
   }
   p.blkStats[b].fetched++;
 }
@@ -823,6 +834,7 @@ __global__ void __launch_bounds__(kMaxBlockThreads, 1) occl_daemon_kernel(const 
   m.cache = reinterpret_cast<CtxSlot*>(smem + kStages * sizeof(Stage));
   m.cacheTag = reinterpret_cast<int*>(m.cache + W);
   m.tq = reinterpret_cast<uint32_t*>(m.cacheTag + W);
+  m.prio = reinterpret_cast<int32_t*>(m.tq + p.maxColl);
   const int tid = threadIdx.x;
   const int b = blockIdx.x - lr * G;
   const int nComputeWarps = (int)(blockDim.x >> 5) - 2;
@@ -838,7 +850,11 @@ __global__ void __launch_bounds__(kMaxBlockThreads, 1) occl_daemon_kernel(const 
     sh.lastRun = -1;
     sh.curId = -1;
     sh.cycRun = sh.cycPoll = sh.cycAcqFence = sh.cycRelFence = sh.nCommit = 0;
-    for (uint32_t i = 0; i < sh.qlen; ++i) m.tq[i] = p.tqSave[(size_t)b * p.maxColl + i];
+    for (uint32_t i = 0; i < sh.qlen; ++i) {
+      m.tq[i] = p.tqSave[(size_t)b * p.maxColl + i];
+      const int c = (int)(m.tq[i] & 0xffffu);
+      m.prio[c] = p.ctx[(size_t)c * G + b].priority;
+    }
     for (int w = 0; w < W; ++w) m.cacheTag[w] = -1;
     sh.lastFetch = globaltimer();
     for (uint32_t i = 0; i < D; ++i) {
@@ -945,7 +961,7 @@ __global__ void __launch_bounds__(kMaxBlockThreads, 1) occl_daemon_kernel(const 
 
 extern "C" size_t occl_internal_daemon_smem(int maxColl, int cacheWays) {
   return (size_t)kStages * sizeof(Stage) + (size_t)cacheWays * sizeof(CtxSlot) + (size_t)cacheWays * sizeof(int) +
-         (size_t)(maxColl + 1) * 4 + 16;
+         (size_t)(maxColl + 1) * 4 + (size_t)maxColl * 4 + 16;
 }
 
 // `pDev` points to a device-memory array of `nranks` parameter blocks (one per

@@ -92,6 +92,7 @@ struct Launcher {
   std::atomic<int> autoLaunch{1};
   std::atomic<int> sticky{0};
   int quitUploaded = -1;                         // effective quitEnabled in paramsDev
+  int lastLaunchQuit = 0;                        // the current/last launch may quit voluntarily
 };
 }  // namespace occl
 
@@ -120,6 +121,7 @@ struct occlComm {
   std::unique_ptr<std::atomic<int>[]> state;     // 0 idle, 1 in flight
   std::vector<occlCallback_t> cb;
   std::vector<void*> cbArg;
+  std::vector<int32_t> prio;                     // per-collective priority (default: collId)
   std::atomic<int> inflight{0};
   // peers
   char* nextArena = nullptr;
@@ -203,6 +205,7 @@ occlResult_t launch_locked(Launcher* L) {
   if ((e = cudaEventRecord(L->evDone, L->stream)) != cudaSuccess) { L->sticky.store((int)e); return occlCudaError; }
   L->launched = true;
   L->launches++;
+  L->lastLaunchQuit = quit;
   return occlSuccess;
 }
 
@@ -234,7 +237,9 @@ void supervisor_main(Launcher* L) {
         if (c->inflight.load() > 0) pending = true;
       }
       pending = pending || newSqe;
-      if (L->autoLaunch.load() && pending && !daemon_running(L) && !L->sticky.load()) {
+      // event-driven start; a launch that could quit voluntarily is always
+      // restarted while work is pending, even if autoLaunch was switched off since
+      if ((L->autoLaunch.load() || L->lastLaunchQuit) && pending && !daemon_running(L) && !L->sticky.load()) {
         // new SQEs start the daemon at once; collectives that are merely stuck
         // (the daemon quit voluntarily) restart after a back-off so that device
         // synchronisation on the host can complete in between
@@ -386,6 +391,7 @@ occlResult_t submit(occlComm* c, int kind, int dtype, int op, int root, size_t c
   e.op = (uint16_t)op;
   e.nblocks = (uint16_t)coll_blocks(c, kind, count, dtype);
   e.root = root;
+  e.priority = c->prio[collId];
   c->state[collId].store(1, std::memory_order_release);
   c->inflight.fetch_add(1);
   return push_sqe(c, e, true);
@@ -487,6 +493,8 @@ occlResult_t occlCommCreate(occlComm_t* out, int nranks, int rank, int cudaDev, 
   for (size_t i = 0; i < M; ++i) c->state[i].store(0);
   c->cb.assign(M, nullptr);
   c->cbArg.assign(M, nullptr);
+  c->prio.resize(M);
+  for (size_t i = 0; i < M; ++i) c->prio[i] = (int32_t)i;
   occlComm* cp = c.get();
   auto fail = [&](cudaError_t) { free_comm(cp); return occlCudaError; };
   cudaError_t e;
@@ -847,6 +855,13 @@ occlResult_t occlGetProbes(occlComm_t c, occlProbes_t* out) {
     out->nData += b.nData;
     out->nCommit += b.nCommit;
   }
+  return occlSuccess;
+}
+
+occlResult_t occlSetPriority(occlComm_t c, int id, int32_t priority) {
+  if (!c || id < 0) return occlInvalidArgument;
+  if (id >= c->cfg.maxColl) return occlRegistryFull;
+  c->prio[id] = priority;
   return occlSuccess;
 }
 

@@ -29,7 +29,8 @@ struct alignas(64) Sqe {
   uint16_t op;
   uint16_t nblocks;    // the collective's grid size
   int32_t root;
-  uint32_t pad[2];
+  int32_t priority;    // user-defined priority (lower runs first) for the priority order policy
+  uint32_t pad;
 };
 static_assert(sizeof(Sqe) == 64, "Sqe must be 64 B");
 
@@ -62,7 +63,8 @@ struct alignas(16) CtxSlot {
   int32_t root;        // meta that also belongs to the static part
   uint16_t nblocks;
   uint16_t nsteps;
-  uint32_t pad[8];
+  int32_t priority;
+  uint32_t pad[7];
 };
 static_assert(sizeof(CtxSlot) == kCtxBytes, "CtxSlot must be 128 B");
 

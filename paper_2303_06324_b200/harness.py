@@ -60,6 +60,9 @@ def timed_batch(comms, jobs, orders=None, timeout_s=600.0):
     orders[local]: permutation of job indices for that rank (default: same order).
     Returns device milliseconds of the single daemon launch that ran them all."""
     dev = comms[0].dev
+    for c in comms:
+        c.set_auto_launch(False)
+    comms[0].quiesce(timeout_s)                       # no event-driven daemon still running
     stream = torch.cuda.ExternalStream(comms[0].stream(), device=dev)
     for li, c in enumerate(comms):
         order = orders[li] if orders is not None else range(len(jobs))
@@ -97,6 +100,7 @@ def host_latency(comms, job, reps=20, timeout_s=60.0):
         ts.append(time.perf_counter() - t0)
     for c in comms:
         c.set_auto_launch(False)
+    comms[0].quiesce(timeout_s)
     ts = sorted(ts[2:])
     return ts[len(ts) // 2] * 1e3
 

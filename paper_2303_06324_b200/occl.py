@@ -34,7 +34,7 @@ EXPORTED = [
     "occlCommInit", "occlCommDestroy", "occlAllReduce", "occlAllGather", "occlReduceScatter",
     "occlBroadcast", "occlWait", "occlTest", "occlSetCallback", "occlGetStats", "occlGetCollStats",
     "occlCommExit", "occlCommLaunch", "occlCommSetAutoLaunch", "occlCommQuiesce", "occlCommGetStream",
-    "occlCollBlocks", "occlCommFuse", "occlGetProbes",
+    "occlCollBlocks", "occlCommFuse", "occlGetProbes", "occlSetPriority",
 ]
 
 
@@ -111,6 +111,7 @@ def _lib():
             "occlCollBlocks": [vp, i, sz, i, C.POINTER(i)],
             "occlCommFuse": [C.POINTER(vp), i],
             "occlGetProbes": [vp, C.POINTER(occlProbes_t)],
+            "occlSetPriority": [vp, i, C.c_int32],
         }.items():
             f = getattr(L, name)
             f.restype = C.c_int
@@ -312,6 +313,9 @@ class Comm:
 
     def coll_stats(self, coll_id):
         return occlGetCollStats(self.h, coll_id)
+
+    def set_priority(self, coll_id, priority):
+        check(_lib().occlSetPriority(self.h, coll_id, priority), "occlSetPriority")
 
     def probes(self) -> dict:
         s = occlProbes_t()

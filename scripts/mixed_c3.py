@@ -57,8 +57,9 @@ def main():
     n = args.ranks
     rows = []
     for wname in args.workloads.split(","):
-        for stick in (1, 0):
-            comms = harness.ring(n, 0, gridBlocks=18, maxColl=256, autoLaunch=0, stickiness=stick)
+        for policy, stick in ((1, 1), (0, 1), (0, 0)):
+            comms = harness.ring(n, 0, gridBlocks=18, maxColl=256, autoLaunch=0, stickiness=stick,
+                                 orderPolicy=policy)
             for seed in range(args.seeds):
                 colls, orders = workload(wname, n, seed)
                 bufs = {c.coll_id: harness.buffers(c.kind, c.dtype, n, c.count, comms) for c in colls}
@@ -68,7 +69,7 @@ def main():
                 ms_r, st_r = run_variant(comms, colls, orders, bufs)
                 nbytes = sum(c.count * harness.ITEM[c.dtype] * (n if c.kind in ("allgather", "reducescatter") else 1)
                              for c in colls)
-                row = {"workload": wname, "stickiness": stick, "seed": seed, "ranks": n, "ncoll": len(colls),
+                row = {"workload": wname, "order_policy": ["fifo", "priority"][policy], "stickiness": stick, "seed": seed, "ranks": n, "ncoll": len(colls),
                        "bytes_per_rank": nbytes, "ms_consistent": ms_c, "ms_random": ms_r,
                        "preemption_overhead": ms_r / ms_c - 1.0,
                        "random": st_r, "consistent": st_c}
