@@ -315,6 +315,7 @@ constexpr int kMaxDepth = 8;           // max slices in flight between control a
 constexpr int kMaxBlockThreads = 576;  // control warp + TMA producer warp + up to 16 compute warps
 constexpr int kTile = 16384;           // TMA staging tile (bytes per operand)
 constexpr int kStages = 6;             // staging ring depth: up to 6 x 2 x 16 KiB of loads in flight
+constexpr int kTmaMinBytes = 16384;    // slices below this use register loads (latency-bound sizes)
 
 // Scheduler state of one block; touched only by the control thread.
 struct Sched {
@@ -354,7 +355,7 @@ __device__ __forceinline__ void save_dyn(CtxSlot* g, const DynCtx& d) {
 
 // Admit an SQE into this block's task queue: write the static context and reset
 // the dynamic cursor (keeping the connector sequence numbers).
-__device__ __noinline__ void admit(const DaemonParams& p, int b, Sched& sh, const Smem& m, const Sqe& e) {
+__device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched& sh, const Smem& m, const Sqe& e) {
   const int G = p.G, n = p.nranks, W = p.cacheWays;
   const int c = (int)e.collId;
   CtxSlot* g = &p.ctx[(size_t)c * G + b];
@@ -382,6 +383,7 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, Sched& sh, cons
   ns->d.kind = e.kind; ns->d.dtype = (uint8_t)e.dtype; ns->d.progressed = 0;
   ns->d.nsent = nsent; ns->d.nrecv = nrecv;
   ns->root = e.root; ns->nblocks = e.nblocks; ns->nsteps = (uint16_t)nsteps; ns->priority = e.priority;
+  ns->lane = (uint32_t)lane;
   uint4* dst = reinterpret_cast<uint4*>(g);
 #pragma unroll
   for (int i = 0; i < kCtxBytes / 16; ++i) st_cg_v4(dst + i, w[i]);
@@ -460,9 +462,15 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
   const bool canFetch = !sh.exiting && qlen < (uint32_t)p.maxColl &&
                         (qlen == 0 || (p.orderPolicy == 0 ? allStalled : (sh.iter % (uint64_t)p.priorityCadence) == 0));
   if (canFetch) {
-    const Sqe* slot = p.sq + (sh.cursor % p.sqDepth);
-    const uint64_t seq = ld_acquire_sys(&slot->seq);
-    if (seq == sh.cursor + 1) {
+    // FIFO fetches one SQE; the priority policy drains what is
+    // there ("checking the SQ more frequently") so that every rank
+    // sorts the same set of collectives as early as possible
+    const int burst = p.orderPolicy == 0 ? 1 : 32;
+    bool fetched = false;
+    for (int k = 0; k < burst && !sh.exiting && sh.qlen < (uint32_t)p.maxColl; ++k) {
+      const Sqe* slot = p.sq + (sh.cursor % p.sqDepth);
+      const uint64_t seq = ld_acquire_sys(&slot->seq);
+      if (seq != sh.cursor + 1) break;
       // the whole 64-B SQE in four 16-B system-scope loads issued back to back
       // (one PCIe round trip instead of one per field)
       uint4 w[4];
@@ -478,10 +486,18 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
       fence_sys();                                   // SQE reads complete before the slot is freed
       st_volatile_u64(&p.sqCursorHost[b], sh.cursor);
       sh.lastFetch = now;
-      if (e.kind == kExit) sh.exiting = 1;          // Exiting SQE
-      else if (b < (int)e.nblocks) admit(p, b, sh, m, e);   // blockIdx < grid size (reading Q11)
-      return CMD_NONE;
+      fetched = true;
+      if (e.kind == kExit) {
+        sh.exiting = 1;                              // Exiting SQE
+      } else {
+        // the collective's blocks start at lane 0 = block (collId mod G), so that
+        // independent small collectives run on different SMs; participate iff
+        // lane < grid size (reading Q11)
+        const int lane = (b - (int)(e.collId % (uint32_t)p.G) + p.G) % p.G;
+        if (lane < (int)e.nblocks) admit(p, b, lane, sh, m, e);
+      }
     }
+    if (fetched) return CMD_NONE;
   }
   const bool stuck = qlen == 0 || allStalled;
   if (qlen == 0 && sh.exiting) {
@@ -588,7 +604,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   Cursor di = dc;
   Cursor dpf = dc;                                        // L2 prefetch cursor (runs ahead of di)
   uint32_t pfAhead = 0;
-  const uint64_t laneLo = (uint64_t)b * part;
+  const uint64_t laneLo = (uint64_t)cx.lane * part;
   uint64_t headSeen = 0, creditSeen = 0;
   uint64_t T = sh.T, spins = 0;
   unsigned long long nSlices = 0, cPoll = 0, cFence = 0;
@@ -753,7 +769,8 @@ __device__ __forceinline__ int tma_vec_bytes(const SliceDesc& d) {
   const int isz = d.dtype == kBF16 ? 2 : 4;
   if (d.nelem <= 0) return 0;
   if ((((uintptr_t)d.src) | ((uintptr_t)d.dst)) & 15) return 0;
-  return (int)((d.nelem * isz) & ~(int64_t)15);
+  const int vb = (int)((d.nelem * isz) & ~(int64_t)15);
+  return vb >= kTmaMinBytes ? vb : 0;          // small slices: lower-latency register path
 }
 
 struct Stage {                 // one staging slot: the incoming operand and the local operand

@@ -64,7 +64,8 @@ struct alignas(16) CtxSlot {
   uint16_t nblocks;
   uint16_t nsteps;
   int32_t priority;
-  uint32_t pad[7];
+  uint32_t lane;       // this block's lane in the collective: (block - collId) mod G
+  uint32_t pad[6];
 };
 static_assert(sizeof(CtxSlot) == kCtxBytes, "CtxSlot must be 128 B");
 

@@ -52,12 +52,16 @@ def main():
     ap.add_argument("--seeds", type=int, default=3)
     ap.add_argument("--workloads", default="c3,resnet50-buckets,resnet50-tensors,bert-large-buckets")
     ap.add_argument("--out", default="gpurun_out/c3_c4")
+    ap.add_argument("--variants", default="priority:1,fifo:1,fifo:0",
+                    help="order_policy:stickiness pairs")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     n = args.ranks
     rows = []
     for wname in args.workloads.split(","):
-        for policy, stick in ((1, 1), (0, 1), (0, 0)):
+        for var in args.variants.split(","):
+            pol, stick = var.split(":")
+            policy, stick = (1 if pol == "priority" else 0), int(stick)
             comms = harness.ring(n, 0, gridBlocks=18, maxColl=256, autoLaunch=0, stickiness=stick,
                                  orderPolicy=policy)
             for seed in range(args.seeds):
