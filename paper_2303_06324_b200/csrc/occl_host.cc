@@ -449,17 +449,17 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->sliceBytes = 64 << 10;
   c->minBlockBytes = 128 << 10;
   c->sqDepth = 1024;
-  c->orderPolicy = occlOrderFifo;
-  c->priorityCadence = 8;
+  c->orderPolicy = occlOrderPriority;   // priority = collId unless set (reading R10)
+  c->priorityCadence = 1;
   c->stickiness = 1;
-  // thresholds in failed connector polls; one poll of an L2-resident flag is
-  // ~0.4-0.5 us on B200, so base ~100 us at the queue front, floor ~4 us,
-  // cap ~2 ms for a collective that keeps making progress (R1)
-  c->spinBase = 256;
-  c->spinStep = 16;
-  c->spinMin = 8;
+  // thresholds in failed connector polls; the daemon's probes measure ~40 ns
+  // per failed poll on B200 (cycPoll / polls), so: queue front ~150 us, floor
+  // ~5 us, cap ~2.5 ms for a collective that keeps making progress (R1)
+  c->spinBase = 4096;
+  c->spinStep = 512;
+  c->spinMin = 128;
   c->spinBoost = 2;
-  c->spinCap = 4096;
+  c->spinCap = 65536;
   c->stallLimit = 2;
   c->quitEnabled = 1;
   c->quitIdleNs = 1'000'000;
