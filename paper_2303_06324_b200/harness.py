@@ -60,6 +60,9 @@ def timed_batch(comms, jobs, orders=None, timeout_s=600.0):
     orders[local]: permutation of job indices for that rank (default: same order).
     Returns device milliseconds of the single daemon launch that ran them all."""
     dev = comms[0].dev
+    # send buffers must hold their data at submission (occl.h conventions,
+    # PAPER.md:525); callers produce them on torch's current stream
+    torch.cuda.current_stream(dev).synchronize()
     for c in comms:
         c.set_auto_launch(False)
     comms[0].quiesce(timeout_s)                       # no event-driven daemon still running

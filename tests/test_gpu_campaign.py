@@ -32,6 +32,9 @@ def test_deadlock_campaign_8_ranks():
                      for _ in range(n)]
                 r = [torch.empty(c.count, dtype=torch.int32, device=0) for _ in range(n)]
                 jobs.append((c.coll_id, "allreduce", "i32", c.count, 0, list(zip(s, r))))
+            # the API contract: send buffers hold their data when the collective is
+            # submitted -- the inputs come from torch's stream
+            torch.cuda.synchronize()
             try:
                 harness.timed_batch(comms, jobs, orders, timeout_s=10.0)
             except occl.OcclError as e:
