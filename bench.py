@@ -47,12 +47,14 @@ def parse():
     ap.add_argument("--ranks", type=int, default=8)
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "i32"])
     ap.add_argument("--grid-blocks", type=int, default=18)
-    ap.add_argument("--slice-kib", type=int, default=64)
+    ap.add_argument("--slice-kib", type=int, default=128)
     ap.add_argument("--conn-slots", type=int, default=4)
     ap.add_argument("--slices-per-chunk", type=int, default=2)
-    ap.add_argument("--threads", type=int, default=576)
+    ap.add_argument("--threads", type=int, default=608)
     ap.add_argument("--pipe-depth", type=int, default=4)
     ap.add_argument("--prefetch", type=int, default=0)
+    ap.add_argument("--discard", type=int, default=1)
+    ap.add_argument("--l2-hints", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--check", action="store_true", help="sampled oracle check of the timed output")
@@ -201,7 +203,8 @@ def make_ring(args, world, prank, dev, dist):
     cfg = occl.occlConfigDefault(gridBlocks=args.grid_blocks, sliceBytes=args.slice_kib * 1024,
                                  connSlots=args.conn_slots, slicesPerChunk=args.slices_per_chunk,
                                  blockThreads=args.threads, pipeDepth=args.pipe_depth,
-                                 prefetchSlices=args.prefetch,
+                                 prefetchSlices=args.prefetch, discardConsumed=args.discard,
+                                 l2Hints=args.l2_hints,
                                  maxColl=128, autoLaunch=0)
     hs = [occl.occlCommCreate(R, prank * V + i, dev, cfg) for i in range(V)]
     mine = [occl.occlCommGetHandle(h) for h in hs]

@@ -75,7 +75,7 @@ typedef enum { occlOrderFifo = 0, occlOrderPriority = 1 } occlOrderPolicy_t;
 typedef struct {
   int maxColl;            /* registry size: collId in [0, maxColl) ("up to 1,000")   */
   int gridBlocks;         /* G: daemon grid = max blocks any collective uses        */
-  int blockThreads;       /* threads per block: control warp + TMA warp + compute warps (96..576)   */
+  int blockThreads;       /* threads per block: control, TMA and publisher warps + compute warps (128..640) */
   int connSlots;          /* K: slots per connector; must exceed slicesPerChunk                    */
   int slicesPerChunk;     /* slices each primitive moves per loop             */
   size_t sliceBytes;      /* bytes per connector slot (multiple of 16)                             */
@@ -97,6 +97,8 @@ typedef struct {
   int cacheWays;          /* direct-mapped shared-memory context cache ways        */
   int pipeDepth;          /* slices in flight between the control warp and the data warps (1..8)   */
   int prefetchSlices;     /* send-buffer slices prefetched into L2 ahead of the issue cursor      */
+  int discardConsumed;    /* 1 = drop consumed connector lines from L2 without write-back         */
+  int l2Hints;            /* 1 = evict-first L2 policy for send/recv-buffer streams               */
 } occlConfig_t;
 
 /* Aggregate counters (device counters summed over blocks/collectives). */

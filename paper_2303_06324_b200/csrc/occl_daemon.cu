@@ -168,20 +168,20 @@ template <> __device__ __forceinline__ uint16_t sadd<kBF16>(uint16_t a, uint16_t
 // persistent kernel must never see a stale line.  The action bits are
 // warp-uniform runtime flags; only the element type is a template.
 template <int DT>
-__device__ __forceinline__ void move_slice(const SliceDesc& d, const int tid, const int nt) {
+__device__ __forceinline__ void move_slice(const int prim, const char* src, const char* cin, char* dst, char* cout,
+                                           const int64_t nelem, const int tid, const int nt) {
   typedef typename Elem<DT>::T T;
   constexpr int A = 16 / sizeof(T);
   constexpr int U = 8;
-  const int prim = d.prim;
   const bool recv = prim & A_RECV, reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
-  const int n = (int)d.nelem;                     // <= sliceBytes / sizeof(T)
+  const int n = (int)nelem;                       // <= sliceBytes / sizeof(T)
   if (n <= 0) return;
-  const bool aligned = ((((uintptr_t)d.src) | ((uintptr_t)d.dst)) & 15) == 0;
+  const bool aligned = ((((uintptr_t)src) | ((uintptr_t)dst)) & 15) == 0;
   const int nvec = aligned ? n / A : 0;
-  const uint4* vs = reinterpret_cast<const uint4*>(d.src);
-  const uint4* vi = reinterpret_cast<const uint4*>(recv ? d.cin : d.src);
-  uint4* vd = reinterpret_cast<uint4*>(d.dst);
-  uint4* vo = reinterpret_cast<uint4*>(d.cout);
+  const uint4* vs = reinterpret_cast<const uint4*>(src);
+  const uint4* vi = reinterpret_cast<const uint4*>(recv ? cin : src);
+  uint4* vd = reinterpret_cast<uint4*>(dst);
+  uint4* vo = reinterpret_cast<uint4*>(cout);
   int i = tid;
   // full tiles: U vectors per thread, no bounds checks
   for (; i + (U - 1) * nt < nvec; i += U * nt) {
@@ -212,22 +212,16 @@ __device__ __forceinline__ void move_slice(const SliceDesc& d, const int tid, co
     if (send) __stcg(vo + i, v);
   }
   // scalar tail (ragged segment ends) or the whole slice when misaligned
-  const T* ss = reinterpret_cast<const T*>(d.src);
-  const T* si = reinterpret_cast<const T*>(recv ? d.cin : d.src);
-  T* sd = reinterpret_cast<T*>(d.dst);
-  T* so = reinterpret_cast<T*>(d.cout);
+  const T* ss = reinterpret_cast<const T*>(src);
+  const T* si = reinterpret_cast<const T*>(recv ? cin : src);
+  T* sd = reinterpret_cast<T*>(dst);
+  T* so = reinterpret_cast<T*>(cout);
   for (int e = nvec * A + tid; e < n; e += nt) {
     T v = __ldcg(si + e);
     if (reduce) v = sadd<DT>(v, __ldcg(ss + e));
     if (copy) sd[e] = v;
     if (send) so[e] = v;
   }
-}
-
-__device__ __forceinline__ void move_slice_any(const SliceDesc& d, const int tid, const int nt) {
-  if (d.dtype == kBF16) move_slice<kBF16>(d, tid, nt);
-  else if (d.dtype == kF32) move_slice<kF32>(d, tid, nt);
-  else move_slice<kI32>(d, tid, nt);
 }
 
 // ------------------------------------------------------------------ ring sequences
@@ -312,7 +306,8 @@ enum : int { CMD_NONE = 0, CMD_RUN = 1, CMD_EXIT = 2 };
 enum : int { RUN_PREEMPT = 0, RUN_GO = 1, RUN_DONE = 2 };
 constexpr int P_EXIT = 0x100;          // descriptor telling the data warps to leave
 constexpr int kMaxDepth = 8;           // max slices in flight between control and data warps
-constexpr int kMaxBlockThreads = 576;  // control warp + TMA producer warp + up to 16 compute warps
+constexpr int kMaxBlockThreads = 640;  // control + TMA producer + publisher warps + up to 17 compute warps
+constexpr int kRoleWarps = 3;          // warps 0..2: control, producer, publisher
 constexpr int kTile = 16384;           // TMA staging tile (bytes per operand)
 constexpr int kStages = 6;             // staging ring depth: up to 6 x 2 x 16 KiB of loads in flight
 constexpr int kTmaMinBytes = 16384;    // slices below this use register loads (latency-bound sizes)
@@ -328,15 +323,19 @@ struct Sched {
 };
 
 // Control -> data warp pipeline: slice descriptors in a ring of `depth` buffers.
-// full[i] completes when the control thread published ring[i]; the data warp
-// that finishes slot i LAST publishes the slice to the peers (release fence +
-// head / credit store) and completes empty[i].  All data warps move slices in
-// order, so slices are published in order and the counters stay monotonic.
+// full[i] completes when the control thread published ring[i]; every compute
+// warp arrives on sdone[i] when it finished its share of the slice; the
+// publisher thread then makes the slice visible to the peers (ONE release fence
+// for every slice finished so far + head / credit store) and completes empty[i].
+// The fence -- an L2 round trip that waits for the SM's outstanding stores --
+// thus never stalls a compute warp (a fenced compute warp would hold back the
+// staging ring for the whole block).  Slices are published in order, so the
+// connector counters stay monotonic.
 struct Pipe {
   SliceDesc ring[kMaxDepth];
-  uint64_t full[kMaxDepth];
-  uint64_t empty[kMaxDepth];     // completes when the slice is moved AND published
-  uint32_t done[kMaxDepth];      // data warps finished with the slot (last one publishes)
+  uint64_t full[kMaxDepth];      // control -> producer / compute / publisher: descriptor valid
+  uint64_t sdone[kMaxDepth];     // compute warps -> publisher: slice moved (count = compute warps)
+  uint64_t empty[kMaxDepth];     // publisher -> control: slice moved AND published
 };
 
 struct Smem {
@@ -755,6 +754,29 @@ __device__ __forceinline__ void tma_load(void* smemDst, const void* gsrc, uint32
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                :: "r"(smem_u32(smemDst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// Same with an L2 cache-eviction policy (user buffers are streamed exactly once:
+// evict-first keeps the connector lines, which are re-read, resident in L2).
+__device__ __forceinline__ void tma_load_hint(void* smemDst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               :: "r"(smem_u32(smemDst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_cg_hint(void* p, const uint4& v, uint64_t pol) {
+  asm volatile("st.global.cg.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
+}
+// Invalidate a consumed connector line in L2 without writing it back: the slot
+// is rewritten by the upstream before anyone reads it again (PTX `discard`
+// behaves like a weak write, so the credit's release orders it before the
+// upstream's next write into the slot).
+__device__ __forceinline__ void discard_l2_line(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" :: "l"(p) : "memory");
+}
 __device__ __forceinline__ uint4 lds_v4(const void* p) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
@@ -765,11 +787,11 @@ __device__ __forceinline__ uint4 lds_v4(const void* p) {
 // A slice goes through the TMA staging ring when its vector part is 16-B aligned
 // (connector slots always are; user buffers almost always).  Otherwise the
 // compute warps move it with register loads (move_slice).
-__device__ __forceinline__ int tma_vec_bytes(const SliceDesc& d) {
-  const int isz = d.dtype == kBF16 ? 2 : 4;
-  if (d.nelem <= 0) return 0;
-  if ((((uintptr_t)d.src) | ((uintptr_t)d.dst)) & 15) return 0;
-  const int vb = (int)((d.nelem * isz) & ~(int64_t)15);
+__device__ __forceinline__ int tma_vec_bytes(int dtype, int64_t nelem, const char* src, const char* dst) {
+  const int isz = dtype == kBF16 ? 2 : 4;
+  if (nelem <= 0) return 0;
+  if ((((uintptr_t)src) | ((uintptr_t)dst)) & 15) return 0;
+  const int vb = (int)((nelem * isz) & ~(int64_t)15);
   return vb >= kTmaMinBytes ? vb : 0;          // small slices: lower-latency register path
 }
 
@@ -783,12 +805,14 @@ struct Stage {                 // one staging slot: the incoming operand and the
 __device__ __noinline__ void producer_main(const DaemonParams& p, Pipe& pipe, Stage* st, uint64_t* tfull,
                                            uint64_t* tempty) {
   const uint32_t D = (uint32_t)p.pipeDepth;
+  const bool hints = p.l2Hints != 0;
+  const uint64_t pol = policy_evict_first();
   uint32_t c = 0;
   for (uint32_t j = 0;; ++j) {
     mbar_wait(&pipe.full[j % D], (j / D) & 1);
     const SliceDesc sd = pipe.ring[j % D];
     if (sd.prim == P_EXIT) break;
-    const int vb = tma_vec_bytes(sd);
+    const int vb = tma_vec_bytes(sd.dtype, sd.nelem, sd.src, sd.dst);
     if (vb == 0) continue;
     // order the acquire of the peer's head (generic proxy) before the bulk reads (async proxy)
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -799,8 +823,12 @@ __device__ __noinline__ void producer_main(const DaemonParams& p, Pipe& pipe, St
       mbar_wait(&tempty[s], (u & 1) ^ 1);
       const uint32_t sz = (uint32_t)min(kTile, vb - off);
       mbar_expect_tx(&tfull[s], reduce ? 2 * sz : sz);
-      tma_load(st[s].in, in + off, sz, &tfull[s]);
-      if (reduce) tma_load(st[s].loc, sd.src + off, sz, &tfull[s]);
+      if (recv || !hints) tma_load(st[s].in, in + off, sz, &tfull[s]);
+      else tma_load_hint(st[s].in, in + off, sz, &tfull[s], pol);
+      if (reduce) {
+        if (hints) tma_load_hint(st[s].loc, sd.src + off, sz, &tfull[s], pol);
+        else tma_load(st[s].loc, sd.src + off, sz, &tfull[s]);
+      }
     }
   }
 }
@@ -808,17 +836,147 @@ __device__ __noinline__ void producer_main(const DaemonParams& p, Pipe& pipe, St
 // Compute warps: reduce / copy the staged tiles into the recv buffer and the
 // downstream connector with 128-bit stores.
 template <int DT>
-__device__ __forceinline__ void consume_tile(const SliceDesc& d, const Stage& s, int off, int sz, int tid, int nt) {
-  const int prim = d.prim;
+__device__ __forceinline__ void consume_tile(const int prim, char* dst, char* cout, const Stage& s, int sz, int tid,
+                                             int nt, bool hints, uint64_t pol) {
   const bool reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
-  uint4* vd = reinterpret_cast<uint4*>(d.dst + off);
-  uint4* vo = reinterpret_cast<uint4*>(d.cout + off);
+  uint4* vd = reinterpret_cast<uint4*>(dst);
+  uint4* vo = reinterpret_cast<uint4*>(cout);
   const int nv = sz >> 4;
   for (int i = tid; i < nv; i += nt) {
     uint4 v = lds_v4(&s.in[i]);
     if (reduce) v = vadd<DT>(v, lds_v4(&s.loc[i]));
-    if (copy) __stcg(vd + i, v);
+    if (copy) {
+      if (hints) st_cg_hint(vd + i, v, pol);
+      else __stcg(vd + i, v);
+    }
     if (send) __stcg(vo + i, v);
+  }
+}
+
+// Compute warps: every compute warp takes part in every slice, in order.  The
+// descriptor is read field by field into registers (a struct copy would live in
+// local memory and be re-read in the inner loop).
+__device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pipe, Stage* stages, uint64_t* tfull,
+                                          uint64_t* tempty, const int ctid, const int cnt) {
+  const uint32_t D = (uint32_t)p.pipeDepth;
+  const int lane = ctid & 31;
+  const bool hints = p.l2Hints != 0, discard = p.discardConsumed != 0;
+  const uint64_t pol = policy_evict_first();
+  const bool leader = ctid == 0;                       // probes
+  unsigned long long cWait = 0, cData = 0, nData = 0;
+  uint32_t c = 0;                                      // staged tiles consumed
+  for (uint32_t j = 0;; ++j) {
+    const uint32_t i = j % D;
+    const long long t0 = clock64();
+    mbar_wait(&pipe.full[i], (j / D) & 1);
+    const SliceDesc* dp = &pipe.ring[i];
+    const int prim = dp->prim;
+    if (prim == P_EXIT) break;
+    const int dtype = dp->dtype;
+    const int64_t nelem = dp->nelem;
+    const char* src = dp->src;
+    const char* cin = dp->cin;
+    char* dst = dp->dst;
+    char* cout = dp->cout;
+    const long long t1 = clock64();
+    const int vb = tma_vec_bytes(dtype, nelem, src, dst);
+    if (vb == 0) {                                     // small or misaligned: register path
+      if (dtype == kBF16) move_slice<kBF16>(prim, src, cin, dst, cout, nelem, ctid, cnt);
+      else if (dtype == kF32) move_slice<kF32>(prim, src, cin, dst, cout, nelem, ctid, cnt);
+      else move_slice<kI32>(prim, src, cin, dst, cout, nelem, ctid, cnt);
+    } else {
+      const bool disc = discard && (prim & A_RECV) && !((uintptr_t)cin & 127);
+      for (int off = 0; off < vb; off += kTile, ++c) {
+        const uint32_t s = c % kStages, u = c / kStages;
+        mbar_wait(&tfull[s], u & 1);
+        const int sz = min(kTile, vb - off);
+        if (disc && ctid < (sz >> 7)) discard_l2_line(cin + off + ((size_t)ctid << 7));  // tile is in smem now
+        if (prim & A_REDUCE) {
+          if (dtype == kF32) consume_tile<kF32>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol);
+          else if (dtype == kBF16) consume_tile<kBF16>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol);
+          else consume_tile<kI32>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol);
+        } else {
+          consume_tile<kI32>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[s]);
+      }
+      // ragged tail (< 16 B) straight from global memory
+      const int isz = dtype == kBF16 ? 2 : 4;
+      const int64_t e0 = vb / isz;
+      const bool rv = prim & A_RECV, rd = prim & A_REDUCE;
+      for (int64_t e = e0 + ctid; e < nelem; e += cnt) {
+        if (isz == 2) {
+          uint16_t v = __ldcg(reinterpret_cast<const uint16_t*>(rv ? cin : src) + e);
+          if (rd) v = sadd<kBF16>(v, __ldcg(reinterpret_cast<const uint16_t*>(src) + e));
+          if (prim & A_COPY) reinterpret_cast<uint16_t*>(dst)[e] = v;
+          if (prim & A_SEND) reinterpret_cast<uint16_t*>(cout)[e] = v;
+        } else {
+          uint32_t v = __ldcg(reinterpret_cast<const uint32_t*>(rv ? cin : src) + e);
+          if (rd) {
+            const uint32_t w = __ldcg(reinterpret_cast<const uint32_t*>(src) + e);
+            v = dtype == kF32 ? __float_as_uint(__fadd_rn(__uint_as_float(v), __uint_as_float(w))) : v + w;
+          }
+          if (prim & A_COPY) reinterpret_cast<uint32_t*>(dst)[e] = v;
+          if (prim & A_SEND) reinterpret_cast<uint32_t*>(cout)[e] = v;
+        }
+      }
+    }
+    // this warp's stores (ordered by __syncwarp) are released to the publisher,
+    // which fences once and raises the peers' flags (publisher_main)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&pipe.sdone[i]);
+    if (leader) {
+      const long long t2 = clock64();
+      cWait += t1 - t0;
+      cData += t2 - t1;
+      ++nData;
+    }
+  }
+  if (leader) {
+    atomicAdd(&p.blkStats[b].cycDataWait, cWait);
+    atomicAdd(&p.blkStats[b].cycData, cData);
+    atomicAdd(&p.blkStats[b].nData, nData);
+  }
+}
+
+// Publisher lane (warp 2 lane 0): makes finished slices visible to the peers in
+// order.  Every slice that is already finished when the publisher gets to it is
+// covered by the same release fence; then the head of the downstream rank and
+// the credit of the upstream rank are raised to the last slice's values
+// (commit visibility).
+__device__ __noinline__ void publisher_main(const DaemonParams& p, Pipe& pipe) {
+  const uint32_t D = (uint32_t)p.pipeDepth;
+  const int sys = p.sysScope;
+  uint32_t j = 0;
+  for (;;) {
+    const uint32_t i = j % D;
+    mbar_wait(&pipe.full[i], (j / D) & 1);
+    if (pipe.ring[i].prim == P_EXIT) break;
+    mbar_wait(&pipe.sdone[i], (j / D) & 1);
+    bool send = false, recv = false;
+    uint64_t hv = 0, cv = 0;
+    char* ho = nullptr;
+    char* co = nullptr;
+    uint32_t k = j;
+    for (;;) {
+      const SliceDesc& d = pipe.ring[k % D];
+      if (d.prim & A_SEND) { send = true; hv = d.headVal; ho = d.headOut; }
+      if (d.prim & A_RECV) { recv = true; cv = d.creditVal; co = d.creditOut; }
+      const uint32_t k1 = k + 1;
+      if (!mbar_test(&pipe.full[k1 % D], (k1 / D) & 1)) break;
+      const SliceDesc& d1 = pipe.ring[k1 % D];
+      if (d1.prim == P_EXIT) break;
+      if ((d1.prim & A_SEND) && ho && d1.headOut != ho) break;
+      if ((d1.prim & A_RECV) && co && d1.creditOut != co) break;
+      if (!mbar_test(&pipe.sdone[k1 % D], (k1 / D) & 1)) break;
+      k = k1;
+    }
+    if (send || recv) fence_acq_rel(sys);
+    if (send) red_max_relaxed(ho, hv, sys);     // head of rank r+1
+    if (recv) red_max_relaxed(co, cv, sys);     // credit of rank r-1
+    for (uint32_t q = j; q <= k; ++q) mbar_arrive(&pipe.empty[q % D]);
+    j = k + 1;
   }
 }
 
@@ -854,7 +1012,7 @@ __global__ void __launch_bounds__(kMaxBlockThreads, 1) occl_daemon_kernel(const 
   m.prio = reinterpret_cast<int32_t*>(m.tq + p.maxColl);
   const int tid = threadIdx.x;
   const int b = blockIdx.x - lr * G;
-  const int nComputeWarps = (int)(blockDim.x >> 5) - 2;
+  const int nComputeWarps = (int)(blockDim.x >> 5) - kRoleWarps;
   const uint32_t D = (uint32_t)p.pipeDepth;
 
   if (tid == 0) {
@@ -876,8 +1034,8 @@ __global__ void __launch_bounds__(kMaxBlockThreads, 1) occl_daemon_kernel(const 
     sh.lastFetch = globaltimer();
     for (uint32_t i = 0; i < D; ++i) {
       mbar_init(&pipe.full[i], 1);
+      mbar_init(&pipe.sdone[i], nComputeWarps);
       mbar_init(&pipe.empty[i], 1);
-      pipe.done[i] = 0;
     }
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&tfull[i], 1);
@@ -888,92 +1046,13 @@ __global__ void __launch_bounds__(kMaxBlockThreads, 1) occl_daemon_kernel(const 
   }
   __syncthreads();
 
-  if (tid < 64) {
+  if (tid < 32 * kRoleWarps) {
     if (tid == 0) control_main(p, b, sh, m, pipe);
     else if (tid == 32) producer_main(p, pipe, stages, tfull, tempty);
+    else if (tid == 64) publisher_main(p, pipe);
     return;
   }
-  // compute warps: every compute warp takes part in every slice, in order
-  const int ctid = tid - 64, cnt = nComputeWarps * 32;
-  const int lane = tid & 31;
-  const bool leader = ctid == 0;                       // probes
-  unsigned long long cWait = 0, cData = 0, nData = 0;
-  uint32_t c = 0;                                      // staged tiles consumed
-  for (uint32_t j = 0;; ++j) {
-    const uint32_t i = j % D;
-    const long long t0 = clock64();
-    mbar_wait(&pipe.full[i], (j / D) & 1);
-    const SliceDesc sd = pipe.ring[i];
-    if (sd.prim == P_EXIT) break;
-    const long long t1 = clock64();
-    const int vb = tma_vec_bytes(sd);
-    if (vb == 0) {
-      move_slice_any(sd, ctid, cnt);                   // misaligned: register path
-    } else {
-      for (int off = 0; off < vb; off += kTile, ++c) {
-        const uint32_t s = c % kStages, u = c / kStages;
-        mbar_wait(&tfull[s], u & 1);
-        const int sz = min(kTile, vb - off);
-        if (sd.prim & A_REDUCE) {
-          if (sd.dtype == kF32) consume_tile<kF32>(sd, stages[s], off, sz, ctid, cnt);
-          else if (sd.dtype == kBF16) consume_tile<kBF16>(sd, stages[s], off, sz, ctid, cnt);
-          else consume_tile<kI32>(sd, stages[s], off, sz, ctid, cnt);
-        } else {
-          consume_tile<kI32>(sd, stages[s], off, sz, ctid, cnt);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[s]);
-      }
-      // ragged tail (< 16 B) straight from global memory
-      const int isz = sd.dtype == kBF16 ? 2 : 4;
-      const int64_t e0 = vb / isz;
-      for (int64_t e = e0 + ctid; e < sd.nelem; e += cnt) {
-        const bool rv = sd.prim & A_RECV, rd = sd.prim & A_REDUCE;
-        if (isz == 2) {
-          uint16_t v = __ldcg(reinterpret_cast<const uint16_t*>(rv ? sd.cin : sd.src) + e);
-          if (rd) v = sadd<kBF16>(v, __ldcg(reinterpret_cast<const uint16_t*>(sd.src) + e));
-          if (sd.prim & A_COPY) reinterpret_cast<uint16_t*>(sd.dst)[e] = v;
-          if (sd.prim & A_SEND) reinterpret_cast<uint16_t*>(sd.cout)[e] = v;
-        } else {
-          uint32_t v = __ldcg(reinterpret_cast<const uint32_t*>(rv ? sd.cin : sd.src) + e);
-          if (rd) {
-            const uint32_t w = __ldcg(reinterpret_cast<const uint32_t*>(sd.src) + e);
-            v = sd.dtype == kF32 ? __float_as_uint(__fadd_rn(__uint_as_float(v), __uint_as_float(w))) : v + w;
-          }
-          if (sd.prim & A_COPY) reinterpret_cast<uint32_t*>(sd.dst)[e] = v;
-          if (sd.prim & A_SEND) reinterpret_cast<uint32_t*>(sd.cout)[e] = v;
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) {
-      // the last compute warp to finish publishes the slice: its acq_rel atomic
-      // observes every other warp's (released) stores, and the fence makes them
-      // visible to the peer before the flag (commit visibility)
-      uint32_t old;
-      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
-                   : "=r"(old) : "r"(smem_u32(&pipe.done[i])) : "memory");
-      if (old == (uint32_t)nComputeWarps - 1) {
-        pipe.done[i] = 0;
-        const int sys = p.sysScope;
-        if (sd.prim & (A_SEND | A_RECV)) fence_acq_rel(sys);
-        if (sd.prim & A_SEND) red_max_relaxed(sd.headOut, sd.headVal, sys);      // head of rank r+1
-        if (sd.prim & A_RECV) red_max_relaxed(sd.creditOut, sd.creditVal, sys);  // credit of rank r-1
-        mbar_arrive(&pipe.empty[i]);
-      }
-    }
-    if (leader) {
-      const long long t2 = clock64();
-      cWait += t1 - t0;
-      cData += t2 - t1;
-      ++nData;
-    }
-  }
-  if (leader) {
-    atomicAdd(&p.blkStats[b].cycDataWait, cWait);
-    atomicAdd(&p.blkStats[b].cycData, cData);
-    atomicAdd(&p.blkStats[b].nData, nData);
-  }
+  compute_main(p, b, pipe, stages, tfull, tempty, tid - 32 * kRoleWarps, nComputeWarps * 32);
 }
 
 extern "C" size_t occl_internal_daemon_smem(int maxColl, int cacheWays) {

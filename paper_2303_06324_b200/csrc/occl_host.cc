@@ -299,7 +299,7 @@ void launcher_stop(Launcher* L) {
 occlResult_t validate_config(const occlConfig_t& c) {
   if (c.maxColl < 1 || c.maxColl > 65535) return occlInvalidArgument;
   if (c.gridBlocks < 1 || c.gridBlocks > 1024) return occlInvalidArgument;
-  if (c.blockThreads < 96 || c.blockThreads > 576 || c.blockThreads % 32) return occlInvalidArgument;
+  if (c.blockThreads < 128 || c.blockThreads > 640 || c.blockThreads % 32) return occlInvalidArgument;
   if (c.slicesPerChunk < 1 || c.connSlots <= c.slicesPerChunk) return occlInvalidArgument;  // invariant I7
   if (c.sliceBytes < 16 || c.sliceBytes % 16 || c.sliceBytes > (1ull << 30)) return occlInvalidArgument;
   if (c.minBlockBytes < 1) return occlInvalidArgument;
@@ -443,10 +443,10 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   std::memset(c, 0, sizeof(*c));
   c->maxColl = 128;
   c->gridBlocks = 16;
-  c->blockThreads = 576;
+  c->blockThreads = 608;                 // 3 role warps + 16 compute warps
   c->connSlots = 4;
   c->slicesPerChunk = 2;
-  c->sliceBytes = 64 << 10;
+  c->sliceBytes = 128 << 10;
   c->minBlockBytes = 128 << 10;
   c->sqDepth = 1024;
   c->orderPolicy = occlOrderPriority;   // priority = collId unless set (reading R10)
@@ -468,6 +468,8 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->cacheWays = 8;
   c->pipeDepth = 4;
   c->prefetchSlices = 0;
+  c->discardConsumed = 1;
+  c->l2Hints = 1;
   return occlSuccess;
 }
 
@@ -635,6 +637,8 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   p.sysScope = c->sysScope;
   p.pipeDepth = c->cfg.pipeDepth;
   p.prefetchSlices = c->cfg.prefetchSlices;
+  p.discardConsumed = c->cfg.discardConsumed;
+  p.l2Hints = c->cfg.l2Hints;
   Launcher* L = new Launcher();
   if ((r = launcher_start(L, {c})) != occlSuccess) {
     launcher_stop(L);

@@ -122,6 +122,8 @@ struct DaemonParams {
   int sysScope;                     // 1: peers in other processes/devices -> .sys fences
   int pipeDepth;                    // slices in flight control -> data warps (<= 8)
   int prefetchSlices;               // L2 prefetch distance for the send-buffer operand (slices)
+  int discardConsumed;              // invalidate consumed connector lines in L2 (no write-back)
+  int l2Hints;                      // evict-first L2 policy for user-buffer loads / stores
 };
 
 }  // namespace occl

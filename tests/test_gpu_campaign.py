@@ -2,7 +2,13 @@
 per-rank submission orders at 8 ranks).  Each trial: 8
 all-reduces of 256 B .. 1 MiB in independent random per-rank orders on 8
 virtual ranks; every trial must complete under a 10 s watchdog and match the
-exact int32 sum (order-free closed form, computed independently with torch)."""
+exact int32 sum (order-free closed form, computed independently with torch).
+
+Two policies: the default priority order (globally agreed priority = collId,
+reading R10 -- the ranks' queues converge on the same front, so misordered
+submissions rarely need a preemption) and the paper's FIFO order with the
+stickiness scheme, where random orders force the daemon to
+preempt, save and resume collectives -- the mechanism under test."""
 import os
 import random
 
@@ -16,15 +22,26 @@ TRIALS = int(os.environ.get("OCCL_CAMPAIGN_TRIALS", "10000"))
 
 
 def test_deadlock_campaign_8_ranks():
+    _campaign(TRIALS, orderPolicy=1)
+
+
+def test_deadlock_campaign_8_ranks_fifo_stickiness():
+    """The paper's policy: FIFO task queues + stickiness; preemptions must occur."""
+    preempt = _campaign(int(os.environ.get("OCCL_CAMPAIGN_FIFO_TRIALS", "1000")), orderPolicy=0, stickiness=1,
+                        spinBase=256, spinStep=32, spinMin=16)
+    assert preempt > 0
+
+
+def _campaign(trials, **cfg):
     if not torch.cuda.is_available():
         pytest.fail("CUDA GPU required")
     from paper_2303_06324_b200 import harness, occl
     n, k = 8, 8
-    comms = harness.ring(n, 0, gridBlocks=4, maxColl=16, sliceBytes=16384, minBlockBytes=65536, autoLaunch=0)
+    comms = harness.ring(n, 0, gridBlocks=4, maxColl=16, sliceBytes=16384, minBlockBytes=65536, autoLaunch=0, **cfg)
     g = torch.Generator(device="cuda")
     timeouts, preempt = 0, 0
     try:
-        for trial in range(TRIALS):
+        for trial in range(trials):
             colls, orders = workloads.deadlock_trial(n, k, seed=trial)
             jobs = []
             for c in colls:
@@ -49,8 +66,9 @@ def test_deadlock_campaign_8_ranks():
         preempt = sum(c.stats()["preemptions"] for c in comms)
     finally:
         occl.destroy_group(comms)
-    print(f"campaign: {TRIALS} trials, {timeouts} timeouts, {preempt} preemptions")
+    print(f"campaign {cfg}: {trials} trials, {timeouts} timeouts, {preempt} preemptions")
     assert timeouts == 0
+    return preempt
 
 
 def _wrap_sum(ts):
