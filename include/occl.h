@@ -99,6 +99,7 @@ typedef struct {
   int prefetchSlices;     /* send-buffer slices prefetched into L2 ahead of the issue cursor      */
   int discardConsumed;    /* 1 = drop consumed connector lines from L2 without write-back         */
   int l2Hints;            /* 1 = evict-first L2 policy for send/recv-buffer streams               */
+  int directMode;         /* 1 = final data goes straight into a same-process peer's recv buffer  */
 } occlConfig_t;
 
 /* Aggregate counters (device counters summed over blocks/collectives). */

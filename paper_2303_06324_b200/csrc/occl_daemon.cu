@@ -121,7 +121,9 @@ template <> __device__ __forceinline__ uint4 vadd<kBF16>(const uint4& a, const u
 
 // ------------------------------------------------------------------ primitives
 // Action bits of the fused primitives.
-enum : int { A_RECV = 1, A_REDUCE = 2, A_COPY = 4, A_SEND = 8 };
+enum : int { A_RECV = 1, A_REDUCE = 2, A_COPY = 4, A_SEND = 8,
+             A_DIN = 16,    // direct receive: the upstream wrote the data into our recv buffer
+             A_DOUT = 32 }; // direct send: write into the downstream's recv buffer, not its connector
 enum : int {
   P_SEND = A_SEND,
   P_RECV = A_RECV | A_COPY,
@@ -176,7 +178,7 @@ __device__ __forceinline__ void move_slice(const int prim, const char* src, cons
   const bool recv = prim & A_RECV, reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
   const int n = (int)nelem;                       // <= sliceBytes / sizeof(T)
   if (n <= 0) return;
-  const bool aligned = ((((uintptr_t)src) | ((uintptr_t)dst)) & 15) == 0;
+  const bool aligned = ((((uintptr_t)src) | ((uintptr_t)dst) | ((uintptr_t)cin) | ((uintptr_t)cout)) & 15) == 0;
   const int nvec = aligned ? n / A : 0;
   const uint4* vs = reinterpret_cast<const uint4*>(src);
   const uint4* vi = reinterpret_cast<const uint4*>(recv ? cin : src);
@@ -259,6 +261,22 @@ __device__ __forceinline__ void step_prim(int kind, int n, int r, int root, int 
       return;
     }
   }
+}
+
+// Direct mode: data that is FINAL -- the all-gather phase of an
+// all-reduce, every hop of an all-gather or broadcast -- goes straight into the
+// downstream's recv buffer instead of its connector (when that buffer is
+// addressable), and a direct receive finds it in place: RecvCopySend becomes a
+// recv-buffer -> peer recv-buffer copy and the final Recv moves no data.  The
+// head / credit protocol is unchanged (a direct message still takes a connector
+// sequence number), so flow control and resume are exactly as before.
+__device__ __forceinline__ int directify(int prim, int kind, int n, int step, bool dOut, bool dIn) {
+  if (n == 1 || kind == kReduceScatter) return prim;
+  const bool agPhase = kind != kAllReduce || step >= n - 1;    // data on the wire is final
+  if (dOut && agPhase && (prim & A_SEND)) prim |= A_DOUT;
+  const bool finalIn = kind != kAllReduce || step >= n;          // received data is final
+  if (dIn && finalIn && (prim & A_RECV)) prim = (prim | A_DIN) & ~A_COPY;  // already in place
+  return prim;
 }
 
 __device__ __forceinline__ int elem_size(int dt) { return dt == kBF16 ? 2 : 4; }
@@ -386,6 +404,13 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched
   uint4* dst = reinterpret_cast<uint4*>(g);
 #pragma unroll
   for (int i = 0; i < kCtxBytes / 16; ++i) st_cg_v4(dst + i, w[i]);
+  if (p.directPrev && n > 1 && e.kind != kReduceScatter) {
+    // tell the upstream where this submission's final data goes (direct mode)
+    char* f = p.flagsPrev + ((size_t)c * G + b) * kFlagStride + kDirectOff;
+    st_relaxed(f, e.recvbuff, p.sysScope);
+    if (p.sysScope) asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(f + 8), "l"(e.subSeq) : "memory");
+    else asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(f + 8), "l"(e.subSeq) : "memory");
+  }
   const int way = c % W;
   if (m.cacheTag[way] == c) m.cacheTag[way] = -1;
   m.prio[c] = e.priority;
@@ -598,6 +623,10 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   char* creditOut = p.flagsPrev + cb * kFlagStride + 128;
   char* connIn = p.dataLocal + cb * K * p.sliceBytes;
   char* connOut = p.dataNext + cb * K * p.sliceBytes;
+  const char* directIn = p.flagsLocal + cb * kFlagStride + kDirectOff;   // {peer recvbuff, subSeq}
+  const bool dOut = p.directNext != 0, dIn = p.directPrev != 0;
+  const uint64_t subSeq = cx.s.subSeq;
+  uint64_t peerRecv = 0;                                  // downstream's recv buffer (direct sends)
   // ---- dynamic context -> registers
   Cursor dc{cx.d.loop, cx.d.step, cx.d.slc, cx.d.nsent, cx.d.nrecv};
   Cursor di = dc;
@@ -631,6 +660,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     // ---- issue the next slice if its connectors are ready
     int prim, seg;
     step_prim(kind, n, r, root, di.step, inplace, prim, seg);
+    prim = directify(prim, kind, n, di.step, dOut, dIn);
     const bool needRecv = prim & A_RECV, needSend = prim & A_SEND;
     bool ok = true;
     const long long tp = clock64();
@@ -641,6 +671,10 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     if (ok && needSend && di.nsent - creditSeen >= (uint64_t)K) {
       creditSeen = ld_acquire(creditIn, sys);
       ok = di.nsent - creditSeen < (uint64_t)K;
+    }
+    if (ok && (prim & A_DOUT) && peerRecv == 0) {         // the downstream admitted this submission?
+      if (ld_acquire(directIn + 8, sys) == subSeq) peerRecv = ld_relaxed(directIn, sys);
+      ok = peerRecv != 0;
     }
     if (!ok) {
       cPoll += clock64() - tp;
@@ -667,8 +701,9 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     SliceDesc& sd = pipe.ring[issued % D];
     sd.src = reinterpret_cast<const char*>(sendbuff) + (sendOff + lo) * isz;
     sd.dst = reinterpret_cast<char*>(recvbuff) + (recvOff + lo) * isz;
-    sd.cin = connIn + (di.nrecv % K) * p.sliceBytes;
-    sd.cout = connOut + (di.nsent % K) * p.sliceBytes;
+    sd.cin = (prim & A_DIN) ? sd.dst : connIn + (di.nrecv % K) * p.sliceBytes;
+    sd.cout = (prim & A_DOUT) ? reinterpret_cast<char*>(peerRecv) + (recvOff + lo) * isz
+                              : connOut + (di.nsent % K) * p.sliceBytes;
     sd.nelem = hi > lo ? (int64_t)(hi - lo) : 0;
     sd.prim = prim;
     sd.dtype = dtype;
@@ -690,6 +725,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
       }
       int pprim, pseg;
       step_prim(kind, n, r, root, dpf.step, inplace, pprim, pseg);
+      pprim = directify(pprim, kind, n, dpf.step, dOut, dIn);
       if ((pprim & A_REDUCE) || !(pprim & A_RECV)) {      // primitive reads the send buffer
         uint64_t so, ro, ln;
         seg_geom(kind, n, r, count, segLen, pseg, so, ro, ln);
@@ -787,10 +823,11 @@ __device__ __forceinline__ uint4 lds_v4(const void* p) {
 // A slice goes through the TMA staging ring when its vector part is 16-B aligned
 // (connector slots always are; user buffers almost always).  Otherwise the
 // compute warps move it with register loads (move_slice).
-__device__ __forceinline__ int tma_vec_bytes(int dtype, int64_t nelem, const char* src, const char* dst) {
+__device__ __forceinline__ int tma_vec_bytes(int dtype, int64_t nelem, const char* src, const char* dst,
+                                             const char* cout) {
   const int isz = dtype == kBF16 ? 2 : 4;
   if (nelem <= 0) return 0;
-  if ((((uintptr_t)src) | ((uintptr_t)dst)) & 15) return 0;
+  if ((((uintptr_t)src) | ((uintptr_t)dst) | ((uintptr_t)cout)) & 15) return 0;   // cout: a peer buffer (direct)
   const int vb = (int)((nelem * isz) & ~(int64_t)15);
   return vb >= kTmaMinBytes ? vb : 0;          // small slices: lower-latency register path
 }
@@ -812,7 +849,8 @@ __device__ __noinline__ void producer_main(const DaemonParams& p, Pipe& pipe, St
     mbar_wait(&pipe.full[j % D], (j / D) & 1);
     const SliceDesc sd = pipe.ring[j % D];
     if (sd.prim == P_EXIT) break;
-    const int vb = tma_vec_bytes(sd.dtype, sd.nelem, sd.src, sd.dst);
+    if (!(sd.prim & (A_COPY | A_SEND))) continue;     // direct final receive: data already in place
+    const int vb = tma_vec_bytes(sd.dtype, sd.nelem, sd.src, sd.dst, sd.cout);
     if (vb == 0) continue;
     // order the acquire of the peer's head (generic proxy) before the bulk reads (async proxy)
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -879,13 +917,15 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
     char* dst = dp->dst;
     char* cout = dp->cout;
     const long long t1 = clock64();
-    const int vb = tma_vec_bytes(dtype, nelem, src, dst);
-    if (vb == 0) {                                     // small or misaligned: register path
+    const int vb = tma_vec_bytes(dtype, nelem, src, dst, cout);
+    if (!(prim & (A_COPY | A_SEND))) {
+      // direct final receive: the data is already in place, nothing to move
+    } else if (vb == 0) {                              // small or misaligned: register path
       if (dtype == kBF16) move_slice<kBF16>(prim, src, cin, dst, cout, nelem, ctid, cnt);
       else if (dtype == kF32) move_slice<kF32>(prim, src, cin, dst, cout, nelem, ctid, cnt);
       else move_slice<kI32>(prim, src, cin, dst, cout, nelem, ctid, cnt);
     } else {
-      const bool disc = discard && (prim & A_RECV) && !((uintptr_t)cin & 127);
+      const bool disc = discard && (prim & A_RECV) && !(prim & A_DIN) && !((uintptr_t)cin & 127);
       for (int off = 0; off < vb; off += kTile, ++c) {
         const uint32_t s = c % kStages, u = c / kStages;
         mbar_wait(&tfull[s], u & 1);

@@ -65,6 +65,7 @@ uint64_t fingerprint(const occlConfig_t& c) {
   auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
   mix(c.maxColl); mix(c.gridBlocks); mix(c.connSlots); mix(c.slicesPerChunk); mix(c.sliceBytes);
   mix(c.minBlockBytes);
+  mix(c.directMode);
   return h;
 }
 
@@ -469,6 +470,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->pipeDepth = 4;
   c->prefetchSlices = 0;
   c->discardConsumed = 1;
+  c->directMode = 1;
   c->l2Hints = 1;
   return occlSuccess;
 }
@@ -594,6 +596,7 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   if ((r = open(hs[next], &c->nextArena, &c->nextIpc)) != occlSuccess) return r;
   if (prev == next) {
     c->prevArena = c->nextArena;
+    c->prevIpc = c->nextIpc;           // closed once, through nextArena (free_comm)
   } else if ((r = open(hs[prev], &c->prevArena, &c->prevIpc)) != occlSuccess) {
     return r;
   }
@@ -638,6 +641,10 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   p.pipeDepth = c->cfg.pipeDepth;
   p.prefetchSlices = c->cfg.prefetchSlices;
   p.discardConsumed = c->cfg.discardConsumed;
+  // direct mode on an edge iff both ends live in this process (raw device
+  // pointers of the peer's buffers are valid here); both ends compute the same
+  p.directNext = c->cfg.directMode && !c->nextIpc;
+  p.directPrev = c->cfg.directMode && !c->prevIpc;
   p.l2Hints = c->cfg.l2Hints;
   Launcher* L = new Launcher();
   if ((r = launcher_start(L, {c})) != occlSuccess) {

@@ -10,7 +10,8 @@ enum Kind : uint16_t { kAllReduce = 0, kAllGather = 1, kReduceScatter = 2, kBroa
 enum Dtype : uint16_t { kI32 = 0, kF32 = 1, kBF16 = 2 };
 
 constexpr int kMaxRanks = 64;
-constexpr int kFlagStride = 256;        // per (coll, block): head @+0, credit @+128 (own lines)
+constexpr int kFlagStride = 384;        // per (coll, block): head @+0, credit @+128, direct @+256 (own lines)
+constexpr int kDirectOff = 256;         // {u64 recvbuff, u64 subSeq} written by the downstream rank
 constexpr int kCtxBytes = 128;          // one context slot (static + dynamic), 16 B aligned
 constexpr int kMaxCacheWays = 32;
 
@@ -123,6 +124,8 @@ struct DaemonParams {
   int pipeDepth;                    // slices in flight control -> data warps (<= 8)
   int prefetchSlices;               // L2 prefetch distance for the send-buffer operand (slices)
   int discardConsumed;              // invalidate consumed connector lines in L2 (no write-back)
+  int directNext;                   // downstream's buffers are addressable: final data goes straight there
+  int directPrev;                   // upstream writes final data straight into our recv buffer
   int l2Hints;                      // evict-first L2 policy for user-buffer loads / stores
 };
 
