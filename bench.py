@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--discard", type=int, default=1)
     ap.add_argument("--l2-hints", type=int, default=1)
     ap.add_argument("--direct", type=int, default=1)
+    ap.add_argument("--stages", type=int, default=6)
+    ap.add_argument("--blocks-per-sm", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--check", action="store_true", help="sampled oracle check of the timed output")
@@ -205,7 +207,8 @@ def make_ring(args, world, prank, dev, dist):
                                  connSlots=args.conn_slots, slicesPerChunk=args.slices_per_chunk,
                                  blockThreads=args.threads, pipeDepth=args.pipe_depth,
                                  prefetchSlices=args.prefetch, discardConsumed=args.discard,
-                                 l2Hints=args.l2_hints, directMode=args.direct,
+                                 l2Hints=args.l2_hints, directMode=args.direct, stagingTiles=args.stages,
+                                 blocksPerSM=args.blocks_per_sm,
                                  maxColl=128, autoLaunch=0)
     hs = [occl.occlCommCreate(R, prank * V + i, dev, cfg) for i in range(V)]
     mine = [occl.occlCommGetHandle(h) for h in hs]

@@ -100,6 +100,8 @@ typedef struct {
   int discardConsumed;    /* 1 = drop consumed connector lines from L2 without write-back         */
   int l2Hints;            /* 1 = evict-first L2 policy for send/recv-buffer streams               */
   int directMode;         /* 1 = final data goes straight into a same-process peer's recv buffer  */
+  int stagingTiles;       /* TMA staging ring depth per block (1..6), 32 KiB of shared memory each */
+  int blocksPerSM;        /* 1 (up to 640 threads) or 2 (up to 384 threads, <= 3 staging tiles)    */
 } occlConfig_t;
 
 /* Aggregate counters (device counters summed over blocks/collectives). */

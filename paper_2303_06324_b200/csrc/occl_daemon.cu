@@ -174,7 +174,7 @@ __device__ __forceinline__ void move_slice(const int prim, const char* src, cons
                                            const int64_t nelem, const int tid, const int nt) {
   typedef typename Elem<DT>::T T;
   constexpr int A = 16 / sizeof(T);
-  constexpr int U = 8;
+  constexpr int U = 2;                            // slices here are < kTmaMinBytes: 2 x 16 B per thread covers them
   const bool recv = prim & A_RECV, reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
   const int n = (int)nelem;                       // <= sliceBytes / sizeof(T)
   if (n <= 0) return;
@@ -327,7 +327,7 @@ constexpr int kMaxDepth = 8;           // max slices in flight between control a
 constexpr int kMaxBlockThreads = 640;  // control + TMA producer + publisher warps + up to 17 compute warps
 constexpr int kRoleWarps = 3;          // warps 0..2: control, producer, publisher
 constexpr int kTile = 16384;           // TMA staging tile (bytes per operand)
-constexpr int kStages = 6;             // staging ring depth: up to 6 x 2 x 16 KiB of loads in flight
+constexpr int kMaxStages = 6;          // staging ring depth: up to 6 x 2 x 16 KiB of loads in flight
 constexpr int kTmaMinBytes = 16384;    // slices below this use register loads (latency-bound sizes)
 
 // Scheduler state of one block; touched only by the control thread.
@@ -838,13 +838,13 @@ struct Stage {                 // one staging slot: the incoming operand and the
 };
 
 // Producer lane (warp 1 lane 0): streams every slice's operands into the staging
-// ring with cp.async.bulk, kStages tiles ahead of the compute warps.
+// ring with cp.async.bulk, p.stages tiles ahead of the compute warps.
 __device__ __noinline__ void producer_main(const DaemonParams& p, Pipe& pipe, Stage* st, uint64_t* tfull,
                                            uint64_t* tempty) {
-  const uint32_t D = (uint32_t)p.pipeDepth;
+  const uint32_t D = (uint32_t)p.pipeDepth, S = (uint32_t)p.stages;
   const bool hints = p.l2Hints != 0;
   const uint64_t pol = policy_evict_first();
-  uint32_t c = 0;
+  uint32_t cs = 0, cph = 0;                          // staging slot and its phase parity
   for (uint32_t j = 0;; ++j) {
     mbar_wait(&pipe.full[j % D], (j / D) & 1);
     const SliceDesc sd = pipe.ring[j % D];
@@ -856,9 +856,10 @@ __device__ __noinline__ void producer_main(const DaemonParams& p, Pipe& pipe, St
     asm volatile("fence.proxy.async.global;" ::: "memory");
     const bool recv = sd.prim & A_RECV, reduce = sd.prim & A_REDUCE;
     const char* in = recv ? sd.cin : sd.src;
-    for (int off = 0; off < vb; off += kTile, ++c) {
-      const uint32_t s = c % kStages, u = c / kStages;
-      mbar_wait(&tempty[s], (u & 1) ^ 1);
+    for (int off = 0; off < vb; off += kTile) {
+      const uint32_t s = cs;
+      mbar_wait(&tempty[s], cph ^ 1);
+      if (++cs == S) { cs = 0; cph ^= 1; }
       const uint32_t sz = (uint32_t)min(kTile, vb - off);
       mbar_expect_tx(&tfull[s], reduce ? 2 * sz : sz);
       if (recv || !hints) tma_load(st[s].in, in + off, sz, &tfull[s]);
@@ -896,13 +897,13 @@ __device__ __forceinline__ void consume_tile(const int prim, char* dst, char* co
 // local memory and be re-read in the inner loop).
 __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pipe, Stage* stages, uint64_t* tfull,
                                           uint64_t* tempty, const int ctid, const int cnt) {
-  const uint32_t D = (uint32_t)p.pipeDepth;
+  const uint32_t D = (uint32_t)p.pipeDepth, S = (uint32_t)p.stages;
   const int lane = ctid & 31;
   const bool hints = p.l2Hints != 0, discard = p.discardConsumed != 0;
   const uint64_t pol = policy_evict_first();
   const bool leader = ctid == 0;                       // probes
   unsigned long long cWait = 0, cData = 0, nData = 0;
-  uint32_t c = 0;                                      // staged tiles consumed
+  uint32_t cs = 0, cph = 0;                            // staging slot and its phase parity
   for (uint32_t j = 0;; ++j) {
     const uint32_t i = j % D;
     const long long t0 = clock64();
@@ -926,9 +927,10 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
       else move_slice<kI32>(prim, src, cin, dst, cout, nelem, ctid, cnt);
     } else {
       const bool disc = discard && (prim & A_RECV) && !(prim & A_DIN) && !((uintptr_t)cin & 127);
-      for (int off = 0; off < vb; off += kTile, ++c) {
-        const uint32_t s = c % kStages, u = c / kStages;
-        mbar_wait(&tfull[s], u & 1);
+      for (int off = 0; off < vb; off += kTile) {
+        const uint32_t s = cs;
+        mbar_wait(&tfull[s], cph);
+        if (++cs == S) { cs = 0; cph ^= 1; }
         const int sz = min(kTile, vb - off);
         if (disc && ctid < (sz >> 7)) discard_l2_line(cin + off + ((size_t)ctid << 7));  // tile is in smem now
         if (prim & A_REDUCE) {
@@ -1036,17 +1038,18 @@ __device__ __noinline__ void publisher_main(const DaemonParams& p, Pipe& pipe) {
 // data warps communicate through a descriptor pipe with mbarriers; the last
 // compute warp to finish a slice publishes it to the peers.
 // =============================================================================
-__global__ void __launch_bounds__(kMaxBlockThreads, 1) occl_daemon_kernel(const DaemonParams* __restrict__ pp, int G) {
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonParams* __restrict__ pp, int G) {
   const int lr = blockIdx.x / G;
   const DaemonParams& p = pp[lr];
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Sched sh;
   __shared__ Pipe pipe;
-  __shared__ uint64_t tfull[kStages], tempty[kStages];
+  __shared__ uint64_t tfull[kMaxStages], tempty[kMaxStages];
   const int W = p.cacheWays;
   Stage* stages = reinterpret_cast<Stage*>(smem);                       // 128-B aligned
   Smem m;
-  m.cache = reinterpret_cast<CtxSlot*>(smem + kStages * sizeof(Stage));
+  m.cache = reinterpret_cast<CtxSlot*>(smem + p.stages * sizeof(Stage));
   m.cacheTag = reinterpret_cast<int*>(m.cache + W);
   m.tq = reinterpret_cast<uint32_t*>(m.cacheTag + W);
   m.prio = reinterpret_cast<int32_t*>(m.tq + p.maxColl);
@@ -1077,7 +1080,7 @@ __global__ void __launch_bounds__(kMaxBlockThreads, 1) occl_daemon_kernel(const 
       mbar_init(&pipe.sdone[i], nComputeWarps);
       mbar_init(&pipe.empty[i], 1);
     }
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < p.stages; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], nComputeWarps);
     }
@@ -1095,21 +1098,35 @@ __global__ void __launch_bounds__(kMaxBlockThreads, 1) occl_daemon_kernel(const 
   compute_main(p, b, pipe, stages, tfull, tempty, tid - 32 * kRoleWarps, nComputeWarps * 32);
 }
 
-extern "C" size_t occl_internal_daemon_smem(int maxColl, int cacheWays) {
-  return (size_t)kStages * sizeof(Stage) + (size_t)cacheWays * sizeof(CtxSlot) + (size_t)cacheWays * sizeof(int) +
+extern "C" size_t occl_internal_daemon_smem(int maxColl, int cacheWays, int stages) {
+  return (size_t)stages * sizeof(Stage) + (size_t)cacheWays * sizeof(CtxSlot) + (size_t)cacheWays * sizeof(int) +
          (size_t)(maxColl + 1) * 4 + (size_t)maxColl * 4 + 16;
+}
+
+// Two builds of the daemon: one block per SM (up to 640 threads) or two blocks
+// per SM (up to 384 threads each, 80 registers) -- two independent schedulers
+// per SM hide each other's ring latency.
+typedef void (*DaemonFn)(const DaemonParams*, int);
+static DaemonFn daemon_fn(int blocksPerSM) {
+  return blocksPerSM >= 2 ? occl_daemon_kernel<384, 2> : occl_daemon_kernel<kMaxBlockThreads, 1>;
 }
 
 // `pDev` points to a device-memory array of `nranks` parameter blocks (one per
 // rank served by this launch, constant for the communicators' lifetime); `p` is
-// the host copy of the first (all share G, maxColl and cacheWays).
+// the host copy of the first (all share G, maxColl and cacheWays).  The daemon is
+// persistent: every block must be resident at once, otherwise blocks that never
+// start would deadlock the ring -- checked against the occupancy calculator.
 extern "C" int occl_internal_launch_daemon(const DaemonParams* p, const DaemonParams* pDev, int nranks,
                                            int blockThreads, void* stream) {
-  const size_t smem = occl_internal_daemon_smem(p->maxColl, p->cacheWays);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(occl_daemon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
-  }
-  occl_daemon_kernel<<<p->G * nranks, blockThreads, smem, (cudaStream_t)stream>>>(pDev, p->G);
+  const size_t smem = occl_internal_daemon_smem(p->maxColl, p->cacheWays, p->stages);
+  DaemonFn fn = daemon_fn(p->blocksPerSM);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  int dev = 0, sms = 0, per = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return (int)e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return (int)e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, blockThreads, smem)) != cudaSuccess) return (int)e;
+  if ((long long)per * sms < (long long)p->G * nranks) return (int)cudaErrorCooperativeLaunchTooLarge;
+  fn<<<p->G * nranks, blockThreads, smem, (cudaStream_t)stream>>>(pDev, p->G);
   return (int)cudaGetLastError();
 }

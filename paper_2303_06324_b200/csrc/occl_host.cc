@@ -311,6 +311,9 @@ occlResult_t validate_config(const occlConfig_t& c) {
   if (c.stallLimit < 1) return occlInvalidArgument;
   if (c.pipeDepth < 1 || c.pipeDepth > 8) return occlInvalidArgument;
   if (c.prefetchSlices < 0 || c.prefetchSlices > 64) return occlInvalidArgument;
+  if (c.stagingTiles < 1 || c.stagingTiles > 6) return occlInvalidArgument;
+  if (c.blocksPerSM < 1 || c.blocksPerSM > 2) return occlInvalidArgument;
+  if (c.blocksPerSM == 2 && (c.blockThreads > 384 || c.stagingTiles > 3)) return occlInvalidArgument;
   return occlSuccess;
 }
 
@@ -471,6 +474,8 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->prefetchSlices = 0;
   c->discardConsumed = 1;
   c->directMode = 1;
+  c->stagingTiles = 6;
+  c->blocksPerSM = 1;
   c->l2Hints = 1;
   return occlSuccess;
 }
@@ -645,6 +650,8 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   // pointers of the peer's buffers are valid here); both ends compute the same
   p.directNext = c->cfg.directMode && !c->nextIpc;
   p.directPrev = c->cfg.directMode && !c->prevIpc;
+  p.stages = c->cfg.stagingTiles;
+  p.blocksPerSM = c->cfg.blocksPerSM;
   p.l2Hints = c->cfg.l2Hints;
   Launcher* L = new Launcher();
   if ((r = launcher_start(L, {c})) != occlSuccess) {
@@ -662,7 +669,8 @@ occlResult_t occlCommFuse(occlComm_t* comms, int n) {
     if (!c || !c->connected || !c->L) return occlInvalidUsage;
     if (c->dev != ms[0]->dev || c->cfg.gridBlocks != ms[0]->cfg.gridBlocks ||
         c->cfg.maxColl != ms[0]->cfg.maxColl || c->cfg.cacheWays != ms[0]->cfg.cacheWays ||
-        c->cfg.blockThreads != ms[0]->cfg.blockThreads || c->cfg.pipeDepth != ms[0]->cfg.pipeDepth)
+        c->cfg.blockThreads != ms[0]->cfg.blockThreads || c->cfg.pipeDepth != ms[0]->cfg.pipeDepth ||
+        c->cfg.stagingTiles != ms[0]->cfg.stagingTiles || c->cfg.blocksPerSM != ms[0]->cfg.blocksPerSM)
       return occlInvalidArgument;
     if (c->L->members.size() != 1) return occlInvalidUsage;   // fuse single-member launchers only
     if (c->inflight.load() > 0) return occlInvalidUsage;

@@ -126,6 +126,8 @@ struct DaemonParams {
   int discardConsumed;              // invalidate consumed connector lines in L2 (no write-back)
   int directNext;                   // downstream's buffers are addressable: final data goes straight there
   int directPrev;                   // upstream writes final data straight into our recv buffer
+  int stages;                       // TMA staging tiles per block (x 2 x 16 KiB of shared memory)
+  int blocksPerSM;                  // 1 or 2 co-resident daemon blocks per SM
   int l2Hints;                      // evict-first L2 policy for user-buffer loads / stores
 };
 
@@ -134,4 +136,4 @@ struct DaemonParams {
 // Launch entry implemented in occl_daemon.cu (internal, not part of the C-ABI).
 extern "C" int occl_internal_launch_daemon(const occl::DaemonParams* p, const occl::DaemonParams* pDev,
                                            int nranks, int blockThreads, void* stream);
-extern "C" size_t occl_internal_daemon_smem(int maxColl, int cacheWays);
+extern "C" size_t occl_internal_daemon_smem(int maxColl, int cacheWays, int stages);
