@@ -102,6 +102,7 @@ typedef struct {
   int directMode;         /* 1 = final data goes straight into a same-process peer's recv buffer  */
   int stagingTiles;       /* TMA staging ring depth per block (1..6), 32 KiB of shared memory each */
   int blocksPerSM;        /* 1 (up to 640 threads) or 2 (up to 384 threads, <= 3 staging tiles)    */
+  uint32_t traceCap;      /* device event-trace records kept per block (0 = tracing off)          */
 } occlConfig_t;
 
 /* Aggregate counters (device counters summed over blocks/collectives). */
@@ -135,6 +136,20 @@ typedef struct {
   uint64_t nData;         /* slices timed by data-group leaders                     */
   uint64_t nCommit;       /* slices committed                                       */
 } occlProbes_t;
+
+/* One device trace record (%globaltimer ns).  tag = event << 24 | collId; for
+ * occlEvPublish the low 16 bits hold the number of slices the fence covered.
+ * arg: Issue = nsent | nrecv << 14 | actions << 28 (connector sequence numbers,
+ *      low 14 bits; actions: 1 recv, 2 reduce, 4 copy, 8 send);
+ * Publish / Sdone (slices moved, before the release fence) = head | credit << 16; SwitchIn / Preempt = task-queue position;
+ * Fetch / Cqe = submission number. */
+typedef struct {
+  uint64_t t;
+  uint32_t tag;
+  uint32_t arg;
+} occlTraceRec_t;
+enum { occlEvFetch = 1, occlEvSwitchIn = 2, occlEvIssue = 3, occlEvPublish = 4, occlEvPreempt = 5,
+       occlEvDone = 6, occlEvCqe = 7, occlEvQuit = 8, occlEvExit = 9, occlEvSdone = 10 };
 
 /* Bootstrap all-gather: gather `bytesPerRank` bytes from every rank into `out`
  * (rank-major).  Return 0 on success. */
@@ -213,6 +228,12 @@ occlResult_t occlSetPriority(occlComm_t comm, int collId, int32_t priority);
 occlResult_t occlGetStats(occlComm_t comm, occlStats_t* out);
 occlResult_t occlGetCollStats(occlComm_t comm, int collId, occlCollStats_t* out);
 occlResult_t occlGetProbes(occlComm_t comm, occlProbes_t* out);
+
+/* Device event trace of block `block` (cfg.traceCap > 0): the most recent
+ * min(written, traceCap) records, oldest first, into out[0..cap); *n = count
+ * copied.  occlTraceReset forgets everything recorded so far (daemon idle). */
+occlResult_t occlGetTrace(occlComm_t comm, int block, occlTraceRec_t* out, size_t cap, size_t* n);
+occlResult_t occlTraceReset(occlComm_t comm);
 
 /* --- daemon control (the paper's lifecycle made explicit) --------------------- */
 /* Push an Exiting SQE: every block drains its task queue, then exits.  A later

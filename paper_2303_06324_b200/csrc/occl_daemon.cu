@@ -319,6 +319,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
                " @!p bra LAB_WAIT_%=;\n}" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
+// ------------------------------------------------------------------ event trace
+// Record slots are claimed with a shared-memory counter (the control and the
+// publisher lanes both trace); the timestamp is taken first so the claim does
+// not skew it.  The publisher writes the block's running count back at exit.
+struct TraceCtl {
+  uint32_t base, idx;
+};
+__device__ __forceinline__ void trace_at(const DaemonParams& p, TraceCtl& tc, int b, uint32_t ev, int coll,
+                                         uint32_t arg) {
+  if (!p.traceCap) return;
+  const uint64_t t = globaltimer();
+  const uint32_t k = tc.base + atomicAdd(&tc.idx, 1u);       // shared-memory atomic
+  TraceRec* r = p.trace + (size_t)b * p.traceCap + (k % p.traceCap);
+  const uint4 v = make_uint4((uint32_t)t, (uint32_t)(t >> 32), (ev << 24) | ((uint32_t)coll & 0xffffu), arg);
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(r), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
 // ------------------------------------------------------------------ shared control
 enum : int { CMD_NONE = 0, CMD_RUN = 1, CMD_EXIT = 2 };
 enum : int { RUN_PREEMPT = 0, RUN_GO = 1, RUN_DONE = 2 };
@@ -354,9 +371,11 @@ struct Pipe {
   uint64_t full[kMaxDepth];      // control -> producer / compute / publisher: descriptor valid
   uint64_t sdone[kMaxDepth];     // compute warps -> publisher: slice moved (count = compute warps)
   uint64_t empty[kMaxDepth];     // publisher -> control: slice moved AND published
+  TraceCtl tr;                   // event-trace slot counter of this block
 };
 
 struct Smem {
+  TraceCtl* tr;        // event-trace slot counter (in the pipe)
   CtxSlot* cache;      // [W]  direct-mapped context cache
   int* cacheTag;       // [W]
   uint32_t* tq;        // [maxColl] task queue: id | stall << 16
@@ -432,6 +451,7 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched
     sh.pos = 0;
   }
   p.blkStats[b].fetched++;
+  trace_at(p, *m.tr, b, kEvFetch, c, (uint32_t)e.subSeq);
 }
 
 // One scheduling round: bookkeeping of the previous run, SQ fetch, entry
@@ -449,6 +469,7 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
       // the CQE.  CQ slot = collId with a single writer, so a
       // release store suffices (R9).
       cs.completions++;
+      trace_at(p, *m.tr, b, kEvDone, id, 0);
       cx.d.progressed = 0;
       save_dyn(g, cx.d);
       fence_acq_rel(1);
@@ -458,6 +479,7 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
         fence_sys();
         st_volatile_u64(&p.cqDone[id], cx.s.subSeq);
         p.blkStats[b].cqes++;
+        trace_at(p, *m.tr, b, kEvCqe, id, (uint32_t)cx.s.subSeq);
       }
       for (uint32_t i = sh.pos; i + 1 < sh.qlen; ++i) m.tq[i] = m.tq[i + 1];
       --sh.qlen;
@@ -470,6 +492,7 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
         cs.ctxSaves++;
       }
       cs.preemptions++;
+      trace_at(p, *m.tr, b, kEvPreempt, id, sh.pos);
       uint32_t st = m.tq[sh.pos] >> 16;
       if (st < 0xffff) ++st;
       m.tq[sh.pos] = (m.tq[sh.pos] & 0xffffu) | (st << 16);
@@ -527,9 +550,11 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
   if (qlen == 0 && sh.exiting) {
     sh.exiting = 0;
     p.blkStats[b].exits++;
+    trace_at(p, *m.tr, b, kEvExit, 0, 0);
     cmd = CMD_EXIT;
   } else if (stuck && p.quitEnabled && now - sh.lastFetch > p.quitIdleNs) {
     p.blkStats[b].quits++;                           // voluntary quit
+    trace_at(p, *m.tr, b, kEvQuit, 0, 0);
     cmd = CMD_EXIT;
   } else if (qlen > 0) {
     const int c = (int)(m.tq[sh.pos] & 0xffffu);
@@ -627,6 +652,9 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   const bool dOut = p.directNext != 0, dIn = p.directPrev != 0;
   const uint64_t subSeq = cx.s.subSeq;
   uint64_t peerRecv = 0;                                  // downstream's recv buffer (direct sends)
+  bool prepared = false;                                  // pipe.ring[issued % D] holds the next slice
+  int curPrim = 0;
+  uint64_t doutOff = 0;
   // ---- dynamic context -> registers
   Cursor dc{cx.d.loop, cx.d.step, cx.d.slc, cx.d.nsent, cx.d.nrecv};
   Cursor di = dc;
@@ -637,6 +665,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   uint64_t T = sh.T, spins = 0;
   unsigned long long nSlices = 0, cPoll = 0, cFence = 0;
   const long long tRun = clock64();
+  trace_at(p, *m.tr, b, kEvSwitchIn, sh.curId, sh.pos);
   int run;
   for (;;) {
     // ---- slices the data warps moved and published: advance the committed cursor
@@ -657,10 +686,36 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
       continue;
     }
     if (issued - committed == D) continue;                // every buffer busy
-    // ---- issue the next slice if its connectors are ready
-    int prim, seg;
-    step_prim(kind, n, r, root, di.step, inplace, prim, seg);
-    prim = directify(prim, kind, n, di.step, dOut, dIn);
+    // ---- prepare the next slice's descriptor BEFORE its connectors are ready,
+    // so that publishing it is a single mbarrier arrive once they are
+    SliceDesc& sd = pipe.ring[issued % D];
+    if (!prepared) {
+      int seg;
+      step_prim(kind, n, r, root, di.step, inplace, curPrim, seg);
+      curPrim = directify(curPrim, kind, n, di.step, dOut, dIn);
+      uint64_t sendOff, recvOff, len;
+      seg_geom(kind, n, r, count, segLen, seg, sendOff, recvOff, len);
+      uint64_t laneHi = laneLo + part;
+      if (laneHi > len) laneHi = len;
+      const uint64_t lo = laneLo + ((uint64_t)di.loop * spc + di.slc) * E;
+      uint64_t hi = lo + E;
+      if (hi > laneHi) hi = laneHi;
+      doutOff = (recvOff + lo) * isz;
+      sd.src = reinterpret_cast<const char*>(sendbuff) + (sendOff + lo) * isz;
+      sd.dst = reinterpret_cast<char*>(recvbuff) + doutOff;
+      sd.cin = (curPrim & A_DIN) ? sd.dst : connIn + (di.nrecv % K) * p.sliceBytes;
+      sd.cout = connOut + (di.nsent % K) * p.sliceBytes;   // direct sends: set once the peer is known
+      sd.nelem = hi > lo ? (int64_t)(hi - lo) : 0;
+      sd.prim = curPrim;
+      sd.dtype = dtype;
+      sd.headOut = headOut;
+      sd.creditOut = creditOut;
+      sd.headVal = di.nsent + 1;
+      sd.creditVal = di.nrecv + 1;
+      prepared = true;
+    }
+    const int prim = curPrim;
+    // ---- issue it if its connectors are ready
     const bool needRecv = prim & A_RECV, needSend = prim & A_SEND;
     bool ok = true;
     const long long tp = clock64();
@@ -685,34 +740,18 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
           ++committed;
           ++nSlices;
         }
-        run = RUN_PREEMPT;
+        run = RUN_PREEMPT;                                // the prepared descriptor is dropped
         break;
       }
       continue;
     }
     spins = 0;
-    uint64_t sendOff, recvOff, len;
-    seg_geom(kind, n, r, count, segLen, seg, sendOff, recvOff, len);
-    uint64_t laneHi = laneLo + part;
-    if (laneHi > len) laneHi = len;
-    const uint64_t lo = laneLo + ((uint64_t)di.loop * spc + di.slc) * E;
-    uint64_t hi = lo + E;
-    if (hi > laneHi) hi = laneHi;
-    SliceDesc& sd = pipe.ring[issued % D];
-    sd.src = reinterpret_cast<const char*>(sendbuff) + (sendOff + lo) * isz;
-    sd.dst = reinterpret_cast<char*>(recvbuff) + (recvOff + lo) * isz;
-    sd.cin = (prim & A_DIN) ? sd.dst : connIn + (di.nrecv % K) * p.sliceBytes;
-    sd.cout = (prim & A_DOUT) ? reinterpret_cast<char*>(peerRecv) + (recvOff + lo) * isz
-                              : connOut + (di.nsent % K) * p.sliceBytes;
-    sd.nelem = hi > lo ? (int64_t)(hi - lo) : 0;
-    sd.prim = prim;
-    sd.dtype = dtype;
-    sd.headOut = headOut;
-    sd.creditOut = creditOut;
-    sd.headVal = di.nsent + 1;
-    sd.creditVal = di.nrecv + 1;
+    if (prim & A_DOUT) sd.cout = reinterpret_cast<char*>(peerRecv) + doutOff;
     mbar_arrive(&pipe.full[issued % D]);
+    trace_at(p, *m.tr, b, kEvIssue, sh.curId,
+          (uint32_t)(di.nsent & 0x3fff) | ((uint32_t)(di.nrecv & 0x3fff) << 14) | ((uint32_t)(prim & 0xf) << 28));
     ++issued;
+    prepared = false;
     advance(di, prim, spc, nsteps);
     if (pfAhead) --pfAhead;
     // ---- prefetch the send-buffer operand of the slices ahead into L2 (TMA
@@ -987,14 +1026,17 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
 // covered by the same release fence; then the head of the downstream rank and
 // the credit of the upstream rank are raised to the last slice's values
 // (commit visibility).
-__device__ __noinline__ void publisher_main(const DaemonParams& p, Pipe& pipe) {
+__device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& pipe) {
   const uint32_t D = (uint32_t)p.pipeDepth;
   const int sys = p.sysScope;
   uint32_t j = 0;
   for (;;) {
     const uint32_t i = j % D;
     mbar_wait(&pipe.full[i], (j / D) & 1);
-    if (pipe.ring[i].prim == P_EXIT) break;
+    if (pipe.ring[i].prim == P_EXIT) {
+      if (p.traceCap) p.traceCount[b] = pipe.tr.base + pipe.tr.idx;   // control traced its last record already
+      break;
+    }
     mbar_wait(&pipe.sdone[i], (j / D) & 1);
     bool send = false, recv = false;
     uint64_t hv = 0, cv = 0;
@@ -1014,9 +1056,11 @@ __device__ __noinline__ void publisher_main(const DaemonParams& p, Pipe& pipe) {
       if (!mbar_test(&pipe.sdone[k1 % D], (k1 / D) & 1)) break;
       k = k1;
     }
+    trace_at(p, pipe.tr, b, kEvSdone, k - j + 1, (uint32_t)(hv & 0xffff) | ((uint32_t)(cv & 0xffff) << 16));
     if (send || recv) fence_acq_rel(sys);
     if (send) red_max_relaxed(ho, hv, sys);     // head of rank r+1
     if (recv) red_max_relaxed(co, cv, sys);     // credit of rank r-1
+    trace_at(p, pipe.tr, b, kEvPublish, k - j + 1, (uint32_t)(hv & 0xffff) | ((uint32_t)(cv & 0xffff) << 16));
     for (uint32_t q = j; q <= k; ++q) mbar_arrive(&pipe.empty[q % D]);
     j = k + 1;
   }
@@ -1053,6 +1097,7 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
   m.cacheTag = reinterpret_cast<int*>(m.cache + W);
   m.tq = reinterpret_cast<uint32_t*>(m.cacheTag + W);
   m.prio = reinterpret_cast<int32_t*>(m.tq + p.maxColl);
+  m.tr = &pipe.tr;
   const int tid = threadIdx.x;
   const int b = blockIdx.x - lr * G;
   const int nComputeWarps = (int)(blockDim.x >> 5) - kRoleWarps;
@@ -1074,6 +1119,8 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
       m.prio[c] = p.ctx[(size_t)c * G + b].priority;
     }
     for (int w = 0; w < W; ++w) m.cacheTag[w] = -1;
+    pipe.tr.base = p.traceCap ? p.traceCount[b] : 0;
+    pipe.tr.idx = 0;
     sh.lastFetch = globaltimer();
     for (uint32_t i = 0; i < D; ++i) {
       mbar_init(&pipe.full[i], 1);
@@ -1092,7 +1139,7 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
   if (tid < 32 * kRoleWarps) {
     if (tid == 0) control_main(p, b, sh, m, pipe);
     else if (tid == 32) producer_main(p, pipe, stages, tfull, tempty);
-    else if (tid == 64) publisher_main(p, pipe);
+    else if (tid == 64) publisher_main(p, b, pipe);
     return;
   }
   compute_main(p, b, pipe, stages, tfull, tempty, tid - 32 * kRoleWarps, nComputeWarps * 32);

@@ -109,6 +109,8 @@ struct occlComm {
   uint32_t* complCnt = nullptr;
   CollStat* collStats = nullptr;
   BlockStat* blkStats = nullptr;
+  TraceRec* trace = nullptr;
+  uint32_t* traceCount = nullptr;
   // pinned + mapped host memory
   Sqe* sqHost = nullptr;
   Sqe* sqDev = nullptr;
@@ -313,6 +315,7 @@ occlResult_t validate_config(const occlConfig_t& c) {
   if (c.prefetchSlices < 0 || c.prefetchSlices > 64) return occlInvalidArgument;
   if (c.stagingTiles < 1 || c.stagingTiles > 6) return occlInvalidArgument;
   if (c.blocksPerSM < 1 || c.blocksPerSM > 2) return occlInvalidArgument;
+  if (c.traceCap > (1u << 24)) return occlInvalidArgument;
   if (c.blocksPerSM == 2 && (c.blockThreads > 384 || c.stagingTiles > 3)) return occlInvalidArgument;
   return occlSuccess;
 }
@@ -411,6 +414,8 @@ void free_comm(occlComm* c) {
   if (c->complCnt) cudaFree(c->complCnt);
   if (c->collStats) cudaFree(c->collStats);
   if (c->blkStats) cudaFree(c->blkStats);
+  if (c->trace) cudaFree(c->trace);
+  if (c->traceCount) cudaFree(c->traceCount);
   if (c->sqHost) cudaFreeHost(c->sqHost);
   if (c->sqCurHost) cudaFreeHost(c->sqCurHost);
   if (c->cqHost) cudaFreeHost(c->cqHost);
@@ -521,6 +526,12 @@ occlResult_t occlCommCreate(occlComm_t* out, int nranks, int rank, int cudaDev, 
   if ((e = cudaMemset(cp->collStats, 0, M * G * sizeof(CollStat))) != cudaSuccess) return fail(e);
   if ((e = cudaMalloc(&cp->blkStats, G * sizeof(BlockStat))) != cudaSuccess) return fail(e);
   if ((e = cudaMemset(cp->blkStats, 0, G * sizeof(BlockStat))) != cudaSuccess) return fail(e);
+  if (cfg.traceCap) {
+    if ((e = cudaMalloc(&cp->trace, G * cfg.traceCap * sizeof(TraceRec))) != cudaSuccess) return fail(e);
+    if ((e = cudaMemset(cp->trace, 0, G * cfg.traceCap * sizeof(TraceRec))) != cudaSuccess) return fail(e);
+  }
+  if ((e = cudaMalloc(&cp->traceCount, G * sizeof(uint32_t))) != cudaSuccess) return fail(e);
+  if ((e = cudaMemset(cp->traceCount, 0, G * sizeof(uint32_t))) != cudaSuccess) return fail(e);
   const unsigned flags = cudaHostAllocMapped | cudaHostAllocPortable;
   if ((e = cudaHostAlloc(&cp->sqHost, cfg.sqDepth * sizeof(Sqe), flags)) != cudaSuccess) return fail(e);
   std::memset(cp->sqHost, 0, cfg.sqDepth * sizeof(Sqe));
@@ -650,6 +661,9 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   // pointers of the peer's buffers are valid here); both ends compute the same
   p.directNext = c->cfg.directMode && !c->nextIpc;
   p.directPrev = c->cfg.directMode && !c->prevIpc;
+  p.trace = c->trace;
+  p.traceCount = c->traceCount;
+  p.traceCap = c->cfg.traceCap;
   p.stages = c->cfg.stagingTiles;
   p.blocksPerSM = c->cfg.blocksPerSM;
   p.l2Hints = c->cfg.l2Hints;
@@ -874,6 +888,43 @@ occlResult_t occlGetProbes(occlComm_t c, occlProbes_t* out) {
     out->nData += b.nData;
     out->nCommit += b.nCommit;
   }
+  return occlSuccess;
+}
+
+occlResult_t occlGetTrace(occlComm_t c, int block, occlTraceRec_t* out, size_t cap, size_t* n) {
+  if (!c || !n || block < 0 || block >= c->cfg.gridBlocks || (cap && !out)) return occlInvalidArgument;
+  *n = 0;
+  if (!c->cfg.traceCap) return occlSuccess;
+  cudaSetDevice(c->dev);
+  uint32_t cnt = 0;
+  const size_t tc = c->cfg.traceCap;
+  std::vector<TraceRec> ring(tc);
+  CUDACHECK(c, cudaMemcpyAsync(&cnt, c->traceCount + block, sizeof(cnt), cudaMemcpyDeviceToHost, c->statsStream));
+  CUDACHECK(c, cudaMemcpyAsync(ring.data(), c->trace + (size_t)block * tc, tc * sizeof(TraceRec),
+                               cudaMemcpyDeviceToHost, c->statsStream));
+  CUDACHECK(c, cudaStreamSynchronize(c->statsStream));
+  const size_t have = cnt < tc ? cnt : tc;
+  const size_t first = cnt - have;                 // oldest record still in the ring
+  size_t k = 0;
+  for (; k < have && k < cap; ++k) {
+    const TraceRec& r = ring[(first + k) % tc];
+    out[k].t = r.t;
+    out[k].tag = r.tag;
+    out[k].arg = r.arg;
+  }
+  *n = k;
+  return occlSuccess;
+}
+
+occlResult_t occlTraceReset(occlComm_t c) {
+  if (!c) return occlInvalidArgument;
+  cudaSetDevice(c->dev);
+  if (c->L) {
+    std::lock_guard<std::mutex> lk(c->L->mu);
+    if (daemon_running(c->L)) return occlInvalidUsage;
+  }
+  CUDACHECK(c, cudaMemsetAsync(c->traceCount, 0, c->cfg.gridBlocks * sizeof(uint32_t), c->statsStream));
+  CUDACHECK(c, cudaStreamSynchronize(c->statsStream));
   return occlSuccess;
 }
 

@@ -96,6 +96,20 @@ struct alignas(16) BlockStat {  // per block
   unsigned long long nCommit;       // slices committed
 };
 
+// Device event trace (one ring of `traceCap` records per block, %globaltimer
+// stamped): slice issue / publish, context switches, preemptions, completions.
+// Used for the paper's context-switch traces and for the
+// per-hop latency analysis of the ring.
+enum TraceEv : uint32_t {
+  kEvFetch = 1, kEvSwitchIn = 2, kEvIssue = 3, kEvPublish = 4, kEvPreempt = 5, kEvDone = 6, kEvCqe = 7,
+  kEvQuit = 8, kEvExit = 9, kEvSdone = 10
+};
+struct alignas(16) TraceRec {
+  uint64_t t;          // %globaltimer (ns)
+  uint32_t tag;        // ev << 24 | collId (16 bits)
+  uint32_t arg;        // event argument (slice sequence, queue position, ...)
+};
+
 struct DaemonParams {
   const Sqe* sq;                    // mapped host SQ
   volatile uint64_t* sqCursorHost;  // mapped host [G]
@@ -126,6 +140,9 @@ struct DaemonParams {
   int discardConsumed;              // invalidate consumed connector lines in L2 (no write-back)
   int directNext;                   // downstream's buffers are addressable: final data goes straight there
   int directPrev;                   // upstream writes final data straight into our recv buffer
+  TraceRec* trace;                  // [G][traceCap] or null
+  uint32_t* traceCount;             // [G] records written (monotonic; ring index = count % traceCap)
+  uint32_t traceCap;
   int stages;                       // TMA staging tiles per block (x 2 x 16 KiB of shared memory)
   int blocksPerSM;                  // 1 or 2 co-resident daemon blocks per SM
   int l2Hints;                      // evict-first L2 policy for user-buffer loads / stores

@@ -34,8 +34,10 @@ EXPORTED = [
     "occlCommInit", "occlCommDestroy", "occlAllReduce", "occlAllGather", "occlReduceScatter",
     "occlBroadcast", "occlWait", "occlTest", "occlSetCallback", "occlGetStats", "occlGetCollStats",
     "occlCommExit", "occlCommLaunch", "occlCommSetAutoLaunch", "occlCommQuiesce", "occlCommGetStream",
-    "occlCollBlocks", "occlCommFuse", "occlGetProbes", "occlSetPriority",
+    "occlCollBlocks", "occlCommFuse", "occlGetProbes", "occlSetPriority", "occlGetTrace", "occlTraceReset",
 ]
+TRACE_EVENTS = {1: "fetch", 2: "switch_in", 3: "issue", 4: "publish", 5: "preempt", 6: "done", 7: "cqe",
+                8: "quit", 9: "exit", 10: "sdone"}
 
 
 class occlConfig_t(C.Structure):
@@ -47,7 +49,7 @@ class occlConfig_t(C.Structure):
         ("spinCap", C.c_uint32), ("stallLimit", C.c_uint32), ("quitEnabled", C.c_int),
         ("quitIdleNs", C.c_uint64), ("idleSleepNs", C.c_uint32), ("autoLaunch", C.c_int), ("cacheWays", C.c_int),
         ("pipeDepth", C.c_int), ("prefetchSlices", C.c_int), ("discardConsumed", C.c_int), ("l2Hints", C.c_int),
-        ("directMode", C.c_int), ("stagingTiles", C.c_int), ("blocksPerSM", C.c_int),
+        ("directMode", C.c_int), ("stagingTiles", C.c_int), ("blocksPerSM", C.c_int), ("traceCap", C.c_uint32),
     ]
 
 
@@ -58,6 +60,10 @@ class occlStats_t(C.Structure):
 
 class occlCollStats_t(C.Structure):
     _fields_ = [(k, C.c_uint64) for k in ("preemptions", "ctxLoads", "ctxSaves", "slices", "completions")]
+
+
+class occlTraceRec_t(C.Structure):
+    _fields_ = [("t", C.c_uint64), ("tag", C.c_uint32), ("arg", C.c_uint32)]
 
 
 class occlProbes_t(C.Structure):
@@ -113,6 +119,8 @@ def _lib():
             "occlCommFuse": [C.POINTER(vp), i],
             "occlGetProbes": [vp, C.POINTER(occlProbes_t)],
             "occlSetPriority": [vp, i, C.c_int32],
+            "occlGetTrace": [vp, i, C.POINTER(occlTraceRec_t), sz, C.POINTER(sz)],
+            "occlTraceReset": [vp],
         }.items():
             f = getattr(L, name)
             f.restype = C.c_int
@@ -322,6 +330,18 @@ class Comm:
         s = occlProbes_t()
         check(_lib().occlGetProbes(self.h, C.byref(s)), "occlGetProbes")
         return {k: getattr(s, k) for k, _ in occlProbes_t._fields_}
+
+    def trace(self, block):
+        """Device event trace of one daemon block: list of (t_ns, event, coll, arg), oldest first."""
+        cap = max(1, int(self.cfg.traceCap))
+        buf = (occlTraceRec_t * cap)()
+        n = C.c_size_t()
+        check(_lib().occlGetTrace(self.h, block, buf, cap, C.byref(n)), "occlGetTrace")
+        return [(buf[k].t, TRACE_EVENTS.get(buf[k].tag >> 24, "?"), buf[k].tag & 0xffff, buf[k].arg)
+                for k in range(n.value)]
+
+    def trace_reset(self):
+        check(_lib().occlTraceReset(self.h), "occlTraceReset")
 
     def destroy(self):
         if self.h:

@@ -106,6 +106,18 @@ __global__ void __launch_bounds__(576, 1) tma_k(const char* a, const char* b, ch
     }
     return;
   }
+  if (tid == 32 && (FX & 8) && !BULK) {
+    // fence-latency probe while the data warps stream stores
+    long long tot = 0; int cnt = 0;
+    const long long t_end = clock64() + 2000000;
+    while (clock64() < t_end) {
+      const long long t0 = clock64();
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      tot += clock64() - t0; ++cnt;
+    }
+    if (blockIdx.x == 0) printf("fence probe (generic stores): %d fences, avg %lld cycles\n", cnt, tot / (cnt ? cnt : 1));
+    return;
+  }
   if (tid == 32) {
     if (!BULK) return;
     // bulk-store issuer: stage s is released once its store has READ the smem
@@ -122,6 +134,17 @@ __global__ void __launch_bounds__(576, 1) tma_k(const char* a, const char* b, ch
     }
     bulk_wait_read<0>();
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    return;
+  }
+  if (tid == 33 && (FX & 8) && BULK) {
+    long long tot = 0; int cnt = 0;
+    const long long t_end = clock64() + 2000000;
+    while (clock64() < t_end) {
+      const long long t0 = clock64();
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      tot += clock64() - t0; ++cnt;
+    }
+    if (blockIdx.x == 0) printf("fence probe (bulk stores): %d fences, avg %lld cycles\n", cnt, tot / (cnt ? cnt : 1));
     return;
   }
   if (tid < 64) return;
@@ -202,28 +225,13 @@ int main() {
   cudaMalloc(&c, bytes);
   cudaMemset(a, 1, bytes);
   cudaMemset(b, 2, bytes);
-  int grids[] = {18, 144};
+  int grids[] = {144, 18};
   for (int g : grids) {
-    auto pr = [&](const char* nm, float ms, int ops) {
-      const double tr = (double)ops * bytes;
-      printf("grid %3d %-22s %.3f ms  %6.0f GB/s  per-CTA %6.1f GB/s\n", g, nm, ms, tr / ms / 1e6, tr / ms / 1e6 / g);
-    };
-    pr("reg-copy U8", run_reg<8, false>(g, a, b, c, bytes), 2);
-    pr("reg-copy U16", run_reg<16, false>(g, a, b, c, bytes), 2);
-    pr("tlds-copy 16Kx6", run_tma<16384, 6, false, false>(g, a, b, c, bytes), 2);
-    pr("tlds-copy 16Kx6 pfence", run_tma<16384, 6, false, false, 1>(g, a, b, c, bytes), 2);
-    pr("tlds-copy 16Kx6 atomcta", run_tma<16384, 6, false, false, 2>(g, a, b, c, bytes), 2);
-    pr("tlds-copy 16Kx6 fencegpu", run_tma<16384, 6, false, false, 4>(g, a, b, c, bytes), 2);
-    pr("tlds-copy 16Kx6 all", run_tma<16384, 6, false, false, 7>(g, a, b, c, bytes), 2);
-    pr("tlds-copy 16Kx12", run_tma<16384, 12, false, false>(g, a, b, c, bytes), 2);
-    pr("tlds-copy 32Kx6", run_tma<32768, 6, false, false>(g, a, b, c, bytes), 2);
-    pr("tbulk-copy 16Kx12", run_tma<16384, 12, false, true>(g, a, b, c, bytes), 2);
-    pr("tbulk-copy 32Kx6", run_tma<32768, 6, false, true>(g, a, b, c, bytes), 2);
-    pr("tbulk-copy 8Kx24", run_tma<8192, 24, false, true>(g, a, b, c, bytes), 2);
-    pr("reg-add U8", run_reg<8, true>(g, a, b, c, bytes), 3);
-    pr("tlds-add 16Kx6", run_tma<16384, 6, true, false>(g, a, b, c, bytes), 3);
-    pr("tbulk-add 16Kx6", run_tma<16384, 6, true, true>(g, a, b, c, bytes), 3);
-    pr("tbulk-add 8Kx12", run_tma<8192, 12, true, true>(g, a, b, c, bytes), 3);
+    printf("grid %d\n", g);
+    run_tma<16384, 6, false, false, 8>(g, a, b, c, bytes);
+    run_tma<16384, 12, false, true, 8>(g, a, b, c, bytes);
+    run_tma<16384, 6, true, false, 8>(g, a, b, c, bytes);
+    run_tma<16384, 6, true, true, 8>(g, a, b, c, bytes);
   }
   return 0;
 }
