@@ -720,7 +720,9 @@ occlResult_t occlCommInit(occlComm_t* out, int nranks, int rank, int cudaDev, oc
 
 occlResult_t occlCommDestroy(occlComm_t c) {
   if (!c) return occlInvalidArgument;
-  if (c->inflight.load() > 0) {
+  // a sticky-errored communicator cannot complete its in-flight work: it may be
+  // destroyed regardless (there is no daemon to drain)
+  if (c->inflight.load() > 0 && !comm_sticky(c)) {
     for (int id = 0; id < c->cfg.maxColl; ++id) try_complete(c, id);
     if (c->inflight.load() > 0) return occlInvalidUsage;
   }
