@@ -189,6 +189,17 @@ occlResult_t occlCommConnect(occlComm_t comm, const void* allHandles, size_t len
  * cacheWays and blockThreads, be idle and have nothing in flight. */
 occlResult_t occlCommFuse(occlComm_t* comms, int n);
 
+/* Sub-communicator (a collective's static context carries its own
+ * nranks / rank, so one daemon per GPU serves collectives of overlapping rank
+ * sets).  `members` lists the parent ranks of the new ring in its rank order;
+ * every member calls this with the same list (globally agreed, like collId) and
+ * the caller must be a member.  The child shares the parent's daemon, SQ, CQ and
+ * collId registry (an id belongs to one communicator at a time); its collectives
+ * use dedicated connectors at (collId, block) in the members' arenas, opened from
+ * the handles the parent received at occlCommConnect.  Destroy children before
+ * their parent.  Up to 31 splits per communicator. */
+occlResult_t occlCommSplit(occlComm_t parent, int nmembers, const int* members, occlComm_t* child);
+
 /* Create + GetHandle + ag(...) + Connect.  The paper's occlCommInit. */
 occlResult_t occlCommInit(occlComm_t* comm, int nranks, int rank, int cudaDev,
                           occlAllGatherFn ag, void* agCtx, const occlConfig_t* cfg);

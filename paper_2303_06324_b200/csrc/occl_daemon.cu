@@ -392,7 +392,8 @@ __device__ __forceinline__ void save_dyn(CtxSlot* g, const DynCtx& d) {
 // Admit an SQE into this block's task queue: write the static context and reset
 // the dynamic cursor (keeping the connector sequence numbers).
 __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched& sh, const Smem& m, const Sqe& e) {
-  const int G = p.G, n = p.nranks, W = p.cacheWays;
+  const RingDesc R = p.rings[e.sub];
+  const int G = p.G, n = R.nranks, W = p.cacheWays;
   const int c = (int)e.collId;
   CtxSlot* g = &p.ctx[(size_t)c * G + b];
   const int isz = elem_size(e.dtype);
@@ -420,12 +421,13 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched
   ns->d.nsent = nsent; ns->d.nrecv = nrecv;
   ns->root = e.root; ns->nblocks = e.nblocks; ns->nsteps = (uint16_t)nsteps; ns->priority = e.priority;
   ns->lane = (uint32_t)lane;
+  ns->sub = e.sub;
   uint4* dst = reinterpret_cast<uint4*>(g);
 #pragma unroll
   for (int i = 0; i < kCtxBytes / 16; ++i) st_cg_v4(dst + i, w[i]);
-  if (p.directPrev && n > 1 && e.kind != kReduceScatter) {
+  if (R.directPrev && n > 1 && e.kind != kReduceScatter) {
     // tell the upstream where this submission's final data goes (direct mode)
-    char* f = p.flagsPrev + ((size_t)c * G + b) * kFlagStride + kDirectOff;
+    char* f = R.flagsPrev + ((size_t)c * G + b) * kFlagStride + kDirectOff;
     st_relaxed(f, e.recvbuff, p.sysScope);
     if (p.sysScope) asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(f + 8), "l"(e.subSeq) : "memory");
     else asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(f + 8), "l"(e.subSeq) : "memory");
@@ -631,8 +633,9 @@ __device__ __forceinline__ void advance(Cursor& d, int prim, int slicesPerChunk,
 __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sched& sh, const Smem& m, Pipe& pipe,
                                               uint32_t& issued, uint32_t& committed) {
   const uint32_t D = (uint32_t)p.pipeDepth;
-  const int n = p.nranks, r = p.rank, K = p.K, sys = p.sysScope, spc = p.slicesPerChunk;
   CtxSlot& cx = m.cache[sh.way];
+  const RingDesc& R = p.rings[cx.sub];                   // the collective's own ring
+  const int n = R.nranks, r = R.rank, K = p.K, sys = p.sysScope, spc = p.slicesPerChunk;
   // ---- static context -> registers
   const uint64_t sendbuff = cx.s.sendbuff, recvbuff = cx.s.recvbuff, count = cx.s.count;
   const uint64_t segLen = cx.s.segLen, part = cx.s.part;
@@ -644,12 +647,12 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   const size_t cb = (size_t)sh.curId * p.G + b;
   const char* headIn = p.flagsLocal + cb * kFlagStride;
   const char* creditIn = headIn + 128;
-  char* headOut = p.flagsNext + cb * kFlagStride;
-  char* creditOut = p.flagsPrev + cb * kFlagStride + 128;
+  char* headOut = R.flagsNext + cb * kFlagStride;
+  char* creditOut = R.flagsPrev + cb * kFlagStride + 128;
   char* connIn = p.dataLocal + cb * K * p.sliceBytes;
-  char* connOut = p.dataNext + cb * K * p.sliceBytes;
+  char* connOut = R.dataNext + cb * K * p.sliceBytes;
   const char* directIn = p.flagsLocal + cb * kFlagStride + kDirectOff;   // {peer recvbuff, subSeq}
-  const bool dOut = p.directNext != 0, dIn = p.directPrev != 0;
+  const bool dOut = R.directNext != 0, dIn = R.directPrev != 0;
   const uint64_t subSeq = cx.s.subSeq;
   uint64_t peerRecv = 0;                                  // downstream's recv buffer (direct sends)
   bool prepared = false;                                  // pipe.ring[issued % D] holds the next slice

@@ -137,7 +137,22 @@ struct occlComm {
   std::mutex sqMu;                               // single submitter: guards the SQ tail
   std::atomic<int> sticky{0};
   occl::Launcher* L = nullptr;                   // daemon lifecycle (own, or shared after occlCommFuse)
+  // sub-communicators (occlCommSplit): a child shares its root's daemon, SQ, CQ
+  // and collId registry and runs its collectives on its own ring (RingDesc)
+  occlComm* parent = nullptr;
+  int sub = 0;                                   // ring index in the root's daemon
+  std::vector<Handle> handles;                   // root: every rank's handle (kept for splits)
+  std::vector<char*> peerArena;                  // root: opened arenas by rank
+  std::vector<char> peerIpc;                     // root: 1 if opened through CUDA IPC
+  RingDesc* ringsDev = nullptr;                  // root: [kMaxRings]
+  int nrings = 0;
+  int children = 0;                              // root: live sub-communicators
+  std::vector<occlComm*> owner;                  // root: per collId, the comm that submitted it
 };
+
+namespace {
+inline occlComm* root_of(occlComm* c) { return c && c->parent ? c->parent : c; }
+}
 
 namespace {
 
@@ -219,6 +234,7 @@ bool try_complete(occlComm* c, int id) {
   int one = 1;
   if (!c->state[id].compare_exchange_strong(one, 0)) return false;
   c->inflight.fetch_sub(1);
+  if (!c->owner.empty() && c->owner[id] && c->owner[id] != c) c->owner[id]->inflight.fetch_sub(1);
   occlCallback_t f = c->cb[id];
   if (f) f(id, c->cbArg[id]);                   // exactly once per completion
   return true;
@@ -369,16 +385,17 @@ occlResult_t push_sqe(occlComm* c, Sqe& e, bool launchNow) {
   return r;
 }
 
-occlResult_t submit(occlComm* c, int kind, int dtype, int op, int root, size_t count, const void* send,
+occlResult_t submit(occlComm* sc, int kind, int dtype, int op, int root, size_t count, const void* send,
                     void* recv, int collId) {
-  if (!c) return occlInvalidArgument;
-  if (!c->connected || !c->L) return occlInvalidUsage;
+  if (!sc) return occlInvalidArgument;
+  occlComm* c = root_of(sc);                          // SQ, CQ and registry of the daemon's owner
+  if (!sc->connected || !c->connected || !c->L) return occlInvalidUsage;
   if (comm_sticky(c)) return occlCudaError;
   if (collId < 0) return occlInvalidArgument;
   if (collId >= c->cfg.maxColl) return occlRegistryFull;
   if (dtype < 0 || dtype > 2) return occlInvalidArgument;
   if (op != occlSum) return occlInvalidArgument;
-  if (kind == kBroadcast && (root < 0 || root >= c->nranks)) return occlInvalidArgument;
+  if (kind == kBroadcast && (root < 0 || root >= sc->nranks)) return occlInvalidArgument;
   if (count > 0 && (!send || !recv)) return occlInvalidArgument;
   if (c->state[collId].load() == 1 && !try_complete(c, collId)) return occlDuplicateSubmit;
   c->subSeq[collId]++;
@@ -388,6 +405,7 @@ occlResult_t submit(occlComm* c, int kind, int dtype, int op, int root, size_t c
     return occlSuccess;
   }
   Sqe e{};
+  e.sub = (uint16_t)sc->sub;
   e.subSeq = c->subSeq[collId];
   e.count = count;
   e.sendbuff = (uint64_t)(uintptr_t)send;
@@ -396,17 +414,20 @@ occlResult_t submit(occlComm* c, int kind, int dtype, int op, int root, size_t c
   e.kind = (uint16_t)kind;
   e.dtype = (uint16_t)dtype;
   e.op = (uint16_t)op;
-  e.nblocks = (uint16_t)coll_blocks(c, kind, count, dtype);
+  e.nblocks = (uint16_t)coll_blocks(sc, kind, count, dtype);   // the collective's own ring size
   e.root = root;
   e.priority = c->prio[collId];
+  c->owner[collId] = sc;
+  if (sc != c) sc->inflight.fetch_add(1);
   c->state[collId].store(1, std::memory_order_release);
   c->inflight.fetch_add(1);
   return push_sqe(c, e, true);
 }
 
 void free_comm(occlComm* c) {
-  if (c->nextIpc && c->nextArena) cudaIpcCloseMemHandle(c->nextArena);
-  if (c->prevIpc && c->prevArena && c->prevArena != c->nextArena) cudaIpcCloseMemHandle(c->prevArena);
+  for (size_t q = 0; q < c->peerArena.size(); ++q)
+    if (c->peerIpc[q] && c->peerArena[q]) cudaIpcCloseMemHandle(c->peerArena[q]);
+  if (c->ringsDev) cudaFree(c->ringsDev);
   if (c->arena) cudaFree(c->arena);
   if (c->ctx) cudaFree(c->ctx);
   if (c->blk) cudaFree(c->blk);
@@ -608,6 +629,9 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
     return occlSuccess;
   };
   const int next = (c->rank + 1) % c->nranks, prev = (c->rank - 1 + c->nranks) % c->nranks;
+  c->handles = hs;
+  c->peerArena.assign(c->nranks, nullptr);
+  c->peerIpc.assign(c->nranks, 0);
   occlResult_t r;
   if ((r = open(hs[next], &c->nextArena, &c->nextIpc)) != occlSuccess) return r;
   if (prev == next) {
@@ -617,6 +641,26 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
     return r;
   }
   c->sysScope = local ? 0 : 1;
+  c->peerArena[next] = c->nextArena;
+  c->peerIpc[next] = c->nextIpc;
+  if (prev != next) {
+    c->peerArena[prev] = c->prevArena;
+    c->peerIpc[prev] = c->prevIpc;
+  }
+  if (c->peerArena[c->rank] == nullptr) c->peerArena[c->rank] = c->arena;   // n == 1: own arena, not opened
+  c->owner.assign(c->cfg.maxColl, nullptr);
+  // ring 0: this communicator's own ring
+  RingDesc rd{};
+  rd.dataNext = c->nextArena;
+  rd.flagsNext = c->nextArena + hs[next].flagsOffset;
+  rd.flagsPrev = c->prevArena + hs[prev].flagsOffset;
+  rd.nranks = c->nranks;
+  rd.rank = c->rank;
+  rd.directNext = c->cfg.directMode && !c->nextIpc;
+  rd.directPrev = c->cfg.directMode && !c->prevIpc;
+  if (cudaMalloc(&c->ringsDev, kMaxRings * sizeof(RingDesc)) != cudaSuccess) return occlCudaError;
+  if (cudaMemcpy(c->ringsDev, &rd, sizeof(rd), cudaMemcpyHostToDevice) != cudaSuccess) return occlCudaError;
+  c->nrings = 1;
   DaemonParams& p = c->params;
   p.sq = c->sqDev;
   p.sqCursorHost = c->sqCurDev;
@@ -661,6 +705,7 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   // pointers of the peer's buffers are valid here); both ends compute the same
   p.directNext = c->cfg.directMode && !c->nextIpc;
   p.directPrev = c->cfg.directMode && !c->prevIpc;
+  p.rings = c->ringsDev;
   p.trace = c->trace;
   p.traceCount = c->traceCount;
   p.traceCap = c->cfg.traceCap;
@@ -680,7 +725,7 @@ occlResult_t occlCommFuse(occlComm_t* comms, int n) {
   if (!comms || n < 1) return occlInvalidArgument;
   std::vector<occlComm*> ms(comms, comms + n);
   for (occlComm* c : ms) {
-    if (!c || !c->connected || !c->L) return occlInvalidUsage;
+    if (!c || !c->connected || !c->L || c->parent || c->children) return occlInvalidUsage;
     if (c->dev != ms[0]->dev || c->cfg.gridBlocks != ms[0]->cfg.gridBlocks ||
         c->cfg.maxColl != ms[0]->cfg.maxColl || c->cfg.cacheWays != ms[0]->cfg.cacheWays ||
         c->cfg.blockThreads != ms[0]->cfg.blockThreads || c->cfg.pipeDepth != ms[0]->cfg.pipeDepth ||
@@ -703,6 +748,73 @@ occlResult_t occlCommFuse(occlComm_t* comms, int n) {
   return r;
 }
 
+occlResult_t occlCommSplit(occlComm_t parent, int nmembers, const int* members, occlComm_t* out) {
+  if (!parent || !members || !out || nmembers < 1) return occlInvalidArgument;
+  occlComm* P = parent;
+  if (P->parent || !P->connected) return occlInvalidUsage;          // split a root communicator
+  if (P->nrings >= kMaxRings) return occlInvalidUsage;
+  std::vector<char> seen(P->nranks, 0);
+  int me = -1;
+  for (int i = 0; i < nmembers; ++i) {
+    const int q = members[i];
+    if (q < 0 || q >= P->nranks || seen[q]) return occlInvalidArgument;
+    seen[q] = 1;
+    if (q == P->rank) me = i;
+  }
+  if (me < 0) return occlInvalidArgument;                            // callers are members
+  cudaSetDevice(P->dev);
+  const int mypid = (int)getpid();
+  const uint64_t myhost = (uint64_t)gethostid();
+  auto peer = [&](int q, char** ptr) -> occlResult_t {              // open (once) the arena of parent rank q
+    if (P->peerArena[q]) { *ptr = P->peerArena[q]; return occlSuccess; }
+    const Handle& h = P->handles[q];
+    if (h.pid == mypid && h.hostId == myhost) {
+      if (h.dev != P->dev) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(h.dev, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (e != cudaSuccess) return cuda_fail(P, e);
+      }
+      P->peerArena[q] = reinterpret_cast<char*>(h.arenaPtr);
+    } else {
+      void* p = nullptr;
+      cudaError_t e = cudaIpcOpenMemHandle(&p, h.ipc, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) return cuda_fail(P, e);
+      P->peerArena[q] = static_cast<char*>(p);
+      P->peerIpc[q] = 1;
+    }
+    *ptr = P->peerArena[q];
+    return occlSuccess;
+  };
+  const int nq = members[(me + 1) % nmembers], pq = members[(me - 1 + nmembers) % nmembers];
+  char *na = nullptr, *pa = nullptr;
+  occlResult_t r;
+  if ((r = peer(nq, &na)) != occlSuccess) return r;
+  if ((r = peer(pq, &pa)) != occlSuccess) return r;
+  RingDesc rd{};
+  rd.dataNext = na;
+  rd.flagsNext = na + P->handles[nq].flagsOffset;
+  rd.flagsPrev = pa + P->handles[pq].flagsOffset;
+  rd.nranks = nmembers;
+  rd.rank = me;
+  rd.directNext = P->cfg.directMode && !P->peerIpc[nq];
+  rd.directPrev = P->cfg.directMode && !P->peerIpc[pq];
+  // the new entry is written before any submission names it (the SQE's release
+  // store orders it for the daemon)
+  if (cudaMemcpy(P->ringsDev + P->nrings, &rd, sizeof(rd), cudaMemcpyHostToDevice) != cudaSuccess)
+    return occlCudaError;
+  occlComm* c = new occlComm();
+  c->parent = P;
+  c->sub = P->nrings++;
+  c->nranks = nmembers;
+  c->rank = me;
+  c->dev = P->dev;
+  c->cfg = P->cfg;
+  c->connected = true;
+  P->children++;
+  *out = c;
+  return occlSuccess;
+}
+
 occlResult_t occlCommInit(occlComm_t* out, int nranks, int rank, int cudaDev, occlAllGatherFn ag, void* agCtx,
                           const occlConfig_t* cfg) {
   if (!out || !ag) return occlInvalidArgument;
@@ -720,6 +832,20 @@ occlResult_t occlCommInit(occlComm_t* out, int nranks, int rank, int cudaDev, oc
 
 occlResult_t occlCommDestroy(occlComm_t c) {
   if (!c) return occlInvalidArgument;
+  if (c->parent) {                                     // sub-communicator: bookkeeping only
+    occlComm* R = c->parent;
+    if (c->inflight.load() > 0 && !comm_sticky(R)) {
+      for (int id = 0; id < R->cfg.maxColl; ++id)
+        if (R->owner[id] == c) try_complete(R, id);
+      if (c->inflight.load() > 0) return occlInvalidUsage;
+    }
+    for (int id = 0; id < R->cfg.maxColl; ++id)
+      if (R->owner[id] == c) R->owner[id] = nullptr;
+    R->children--;
+    delete c;
+    return occlSuccess;
+  }
+  if (c->children > 0) return occlInvalidUsage;        // destroy the sub-communicators first
   // a sticky-errored communicator cannot complete its in-flight work: it may be
   // destroyed regardless (there is no daemon to drain)
   if (c->inflight.load() > 0 && !comm_sticky(c)) {
@@ -778,6 +904,7 @@ occlResult_t occlBroadcast(const void* s, void* r, size_t count, occlDataType_t 
 }
 
 occlResult_t occlTest(occlComm_t c, int id, int* done) {
+  c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c || !done || id < 0) return occlInvalidArgument;
   if (id >= c->cfg.maxColl) return occlRegistryFull;
   if (c->subSeq[id] == 0) return occlUnknownId;
@@ -788,6 +915,7 @@ occlResult_t occlTest(occlComm_t c, int id, int* done) {
 }
 
 occlResult_t occlWait(occlComm_t c, int id, int64_t timeoutNs) {
+  c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c || id < 0) return occlInvalidArgument;
   if (id >= c->cfg.maxColl) return occlRegistryFull;
   if (c->subSeq[id] == 0) return occlUnknownId;
@@ -812,6 +940,7 @@ occlResult_t occlWait(occlComm_t c, int id, int64_t timeoutNs) {
 }
 
 occlResult_t occlSetCallback(occlComm_t c, int id, occlCallback_t cb, void* arg) {
+  c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c || id < 0) return occlInvalidArgument;
   if (id >= c->cfg.maxColl) return occlRegistryFull;
   if (c->state[id].load() == 1) return occlInvalidUsage;   // rebinding only between submissions
@@ -821,6 +950,7 @@ occlResult_t occlSetCallback(occlComm_t c, int id, occlCallback_t cb, void* arg)
 }
 
 occlResult_t occlGetStats(occlComm_t c, occlStats_t* out) {
+  c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c || !out) return occlInvalidArgument;
   std::memset(out, 0, sizeof(*out));
   const size_t M = c->cfg.maxColl, G = c->cfg.gridBlocks;
@@ -853,6 +983,7 @@ occlResult_t occlGetStats(occlComm_t c, occlStats_t* out) {
 }
 
 occlResult_t occlGetCollStats(occlComm_t c, int id, occlCollStats_t* out) {
+  c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c || !out || id < 0) return occlInvalidArgument;
   if (id >= c->cfg.maxColl) return occlRegistryFull;
   const size_t G = c->cfg.gridBlocks;
@@ -873,6 +1004,7 @@ occlResult_t occlGetCollStats(occlComm_t c, int id, occlCollStats_t* out) {
 }
 
 occlResult_t occlGetProbes(occlComm_t c, occlProbes_t* out) {
+  c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c || !out) return occlInvalidArgument;
   const size_t G = c->cfg.gridBlocks;
   std::vector<BlockStat> bs(G);
@@ -894,6 +1026,7 @@ occlResult_t occlGetProbes(occlComm_t c, occlProbes_t* out) {
 }
 
 occlResult_t occlGetTrace(occlComm_t c, int block, occlTraceRec_t* out, size_t cap, size_t* n) {
+  c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c || !n || block < 0 || block >= c->cfg.gridBlocks || (cap && !out)) return occlInvalidArgument;
   *n = 0;
   if (!c->cfg.traceCap) return occlSuccess;
@@ -919,6 +1052,7 @@ occlResult_t occlGetTrace(occlComm_t c, int block, occlTraceRec_t* out, size_t c
 }
 
 occlResult_t occlTraceReset(occlComm_t c) {
+  c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c) return occlInvalidArgument;
   cudaSetDevice(c->dev);
   if (c->L) {
@@ -931,6 +1065,7 @@ occlResult_t occlTraceReset(occlComm_t c) {
 }
 
 occlResult_t occlSetPriority(occlComm_t c, int id, int32_t priority) {
+  c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c || id < 0) return occlInvalidArgument;
   if (id >= c->cfg.maxColl) return occlRegistryFull;
   c->prio[id] = priority;
@@ -938,6 +1073,7 @@ occlResult_t occlSetPriority(occlComm_t c, int id, int32_t priority) {
 }
 
 occlResult_t occlCommExit(occlComm_t c) {
+  c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c) return occlInvalidArgument;
   if (!c->connected || !c->L) return occlInvalidUsage;
   Sqe e{};
@@ -946,6 +1082,7 @@ occlResult_t occlCommExit(occlComm_t c) {
 }
 
 occlResult_t occlCommLaunch(occlComm_t c) {
+  c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c) return occlInvalidArgument;
   if (!c->connected || !c->L) return occlInvalidUsage;
   cudaSetDevice(c->dev);
@@ -954,6 +1091,7 @@ occlResult_t occlCommLaunch(occlComm_t c) {
 }
 
 occlResult_t occlCommSetAutoLaunch(occlComm_t c, int enable) {
+  c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c || !c->L) return occlInvalidArgument;
   c->L->autoLaunch.store(enable ? 1 : 0);
   c->L->cv.notify_one();
@@ -961,6 +1099,7 @@ occlResult_t occlCommSetAutoLaunch(occlComm_t c, int enable) {
 }
 
 occlResult_t occlCommQuiesce(occlComm_t c, int64_t timeoutNs) {
+  c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c || !c->L) return occlInvalidArgument;
   const uint64_t t0 = now_ns();
   for (;;) {
@@ -974,6 +1113,7 @@ occlResult_t occlCommQuiesce(occlComm_t c, int64_t timeoutNs) {
 }
 
 occlResult_t occlCommGetStream(occlComm_t c, void** stream) {
+  c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c || !stream || !c->L) return occlInvalidArgument;
   *stream = (void*)c->L->stream;
   return occlSuccess;

@@ -31,9 +31,23 @@ struct alignas(64) Sqe {
   uint16_t nblocks;    // the collective's grid size
   int32_t root;
   int32_t priority;    // user-defined priority (lower runs first) for the priority order policy
-  uint32_t pad;
+  uint16_t sub;        // ring of this rank's daemon the collective runs on (0: the communicator,
+                       // k: its k-th sub-communicator, occlCommSplit); local to this rank
+  uint16_t pad;
 };
 static_assert(sizeof(Sqe) == 64, "Sqe must be 64 B");
+
+constexpr int kMaxRings = 32;           // communicator + sub-communicators served by one daemon
+// One ring the daemon serves (the static context carries the
+// collective's own nranks / rank).  Connectors and flags of a collective live at
+// (collId, block) in every member's arena, so only the neighbours differ.
+struct alignas(16) RingDesc {
+  char* dataNext;      // downstream member's connector data
+  char* flagsNext;     // downstream member's flags
+  char* flagsPrev;     // upstream member's flags
+  int32_t nranks, rank;
+  int32_t directNext, directPrev;
+};
 
 // Static context: constant for one submission.  48 B.
 struct alignas(16) StaticCtx {
@@ -66,7 +80,8 @@ struct alignas(16) CtxSlot {
   uint16_t nsteps;
   int32_t priority;
   uint32_t lane;       // this block's lane in the collective: (block - collId) mod G
-  uint32_t pad[6];
+  uint32_t sub;        // ring (RingDesc index) of the collective
+  uint32_t pad[5];
 };
 static_assert(sizeof(CtxSlot) == kCtxBytes, "CtxSlot must be 128 B");
 
@@ -140,6 +155,7 @@ struct DaemonParams {
   int discardConsumed;              // invalidate consumed connector lines in L2 (no write-back)
   int directNext;                   // downstream's buffers are addressable: final data goes straight there
   int directPrev;                   // upstream writes final data straight into our recv buffer
+  const RingDesc* rings;            // [kMaxRings] ring 0 = this communicator, then sub-communicators
   TraceRec* trace;                  // [G][traceCap] or null
   uint32_t* traceCount;             // [G] records written (monotonic; ring index = count % traceCap)
   uint32_t traceCap;

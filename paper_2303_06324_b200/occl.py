@@ -35,6 +35,7 @@ EXPORTED = [
     "occlBroadcast", "occlWait", "occlTest", "occlSetCallback", "occlGetStats", "occlGetCollStats",
     "occlCommExit", "occlCommLaunch", "occlCommSetAutoLaunch", "occlCommQuiesce", "occlCommGetStream",
     "occlCollBlocks", "occlCommFuse", "occlGetProbes", "occlSetPriority", "occlGetTrace", "occlTraceReset",
+    "occlCommSplit",
 ]
 TRACE_EVENTS = {1: "fetch", 2: "switch_in", 3: "issue", 4: "publish", 5: "preempt", 6: "done", 7: "cqe",
                 8: "quit", 9: "exit", 10: "sdone"}
@@ -121,6 +122,7 @@ def _lib():
             "occlSetPriority": [vp, i, C.c_int32],
             "occlGetTrace": [vp, i, C.POINTER(occlTraceRec_t), sz, C.POINTER(sz)],
             "occlTraceReset": [vp],
+            "occlCommSplit": [vp, i, C.POINTER(i), C.POINTER(vp)],
         }.items():
             f = getattr(L, name)
             f.restype = C.c_int
@@ -331,6 +333,14 @@ class Comm:
         check(_lib().occlGetProbes(self.h, C.byref(s)), "occlGetProbes")
         return {k: getattr(s, k) for k, _ in occlProbes_t._fields_}
 
+    def split(self, members):
+        """Sub-communicator over parent ranks `members` (in the new ring's order);
+        shares this communicator's daemon (occlCommSplit)."""
+        arr = (C.c_int * len(members))(*members)
+        h = C.c_void_p()
+        check(_lib().occlCommSplit(self.h, len(members), arr, C.byref(h)), "occlCommSplit")
+        return Comm(h.value, len(members), list(members).index(self.rank), self.dev, self.cfg)
+
     def trace(self, block):
         """Device event trace of one daemon block: list of (t_ns, event, coll, arg), oldest first."""
         cap = max(1, int(self.cfg.traceCap))
@@ -388,6 +398,16 @@ def process_group(pg=None, device=None, cfg=None, **overrides):
     dist.all_gather_object(allh, mine, group=pg)
     occlCommConnect(h, allh)
     return Comm(h, n, rank, device, cfg)
+
+
+def split_group(comms, groups):
+    """Split every rank of a local group into the sub-communicator of the group
+    (list of parent ranks) it belongs to; returns {group index: [child comms in
+    child-rank order]}."""
+    out = {}
+    for gi, g in enumerate(groups):
+        out[gi] = [comms[q].split(g) for q in g]
+    return out
 
 
 def destroy_group(comms):
