@@ -52,6 +52,12 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const void* p) {
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint64_t ld_acquire(const void* p, int sys) {
+  uint64_t v;
+  if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_relaxed(void* p, uint64_t v, int sys) {
   if (sys) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
   else     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
@@ -334,6 +340,7 @@ __device__ __forceinline__ void trace_at(const DaemonParams& p, TraceCtl& tc, in
   TraceRec* r = p.trace + (size_t)b * p.traceCap + (k % p.traceCap);
   const uint4 v = make_uint4((uint32_t)t, (uint32_t)(t >> 32), (ev << 24) | ((uint32_t)coll & 0xffffu), arg);
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(r), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+  atomicMax(&p.traceCount[b], k + 1);                          // readable while the daemon runs
 }
 
 // ------------------------------------------------------------------ shared control
@@ -456,6 +463,44 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched
   trace_at(p, *m.tr, b, kEvFetch, c, (uint32_t)e.subSeq);
 }
 
+// SQ fetch through a device-memory mirror.  Every block consumes
+// every SQE, but only the block holding `fetchLock` reads the
+// host SQ over PCIe: it copies new SQEs into the mirror (as long as no block
+// still needs the slot it overwrites), publishes the mirror tail, and tells the
+// host which SQ slots are free.  The other blocks read the mirror from L2.  This
+// replaces G PCIe reads per SQE (and per idle poll) with one.
+__device__ __noinline__ void sq_fetch(const DaemonParams& p) {
+  if (atomicCAS(p.fetchLock, 0u, 1u) != 0u) return;            // another block is fetching
+  uint64_t t = ld_relaxed(p.mirrorTail, 0);
+  uint64_t minCur = ~0ull;
+  for (int bb = 0; bb < p.G; ++bb) {
+    uint64_t c;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(c) : "l"(&p.blk[bb].sqCursor) : "memory");
+    minCur = c < minCur ? c : minCur;
+  }
+  const uint64_t t0 = t;
+  while (t - minCur < p.sqDepth && t - t0 < 64) {
+    const Sqe* slot = p.sq + (t % p.sqDepth);
+    if (ld_acquire_sys(&slot->seq) != t + 1) break;            // written last by the host (release)
+    uint4 w[4];
+    const char* base = reinterpret_cast<const char*>(slot);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      asm volatile("ld.relaxed.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(w[q].x), "=r"(w[q].y), "=r"(w[q].z), "=r"(w[q].w) : "l"(base + 16 * q) : "memory");
+    uint4* dst = reinterpret_cast<uint4*>(p.sqMirror + (t % p.sqDepth));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) st_cg_v4(dst + q, w[q]);
+    ++t;
+  }
+  if (t != t0) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(p.mirrorTail), "l"(t) : "memory");
+    fence_sys();                                               // host SQE reads done before the slots are freed
+    st_volatile_u64(&p.sqCursorHost[0], t);
+  }
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p.fetchLock), "r"(0u) : "memory");
+}
+
 // One scheduling round: bookkeeping of the previous run, SQ fetch, entry
 // selection, voluntary quit.  Returns CMD_*.
 __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, const Smem& m) {
@@ -474,7 +519,7 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
       trace_at(p, *m.tr, b, kEvDone, id, 0);
       cx.d.progressed = 0;
       save_dyn(g, cx.d);
-      fence_acq_rel(1);
+      fence_acq_rel(0);                               // gpu scope: the CQE writer's fence.sys is cumulative
       const uint32_t old = atom_add_acq_rel(&p.complCnt[id], 1u);
       if (old + 1 == cx.nblocks) {
         p.complCnt[id] = 0;
@@ -516,24 +561,22 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
     // sorts the same set of collectives as early as possible
     const int burst = p.orderPolicy == 0 ? 1 : 32;
     bool fetched = false;
-    for (int k = 0; k < burst && !sh.exiting && sh.qlen < (uint32_t)p.maxColl; ++k) {
-      const Sqe* slot = p.sq + (sh.cursor % p.sqDepth);
-      const uint64_t seq = ld_acquire_sys(&slot->seq);
-      if (seq != sh.cursor + 1) break;
-      // the whole 64-B SQE in four 16-B system-scope loads issued back to back
-      // (one PCIe round trip instead of one per field)
+    uint64_t tail = ld_acquire(p.mirrorTail, 0);
+    if (tail <= sh.cursor) {
+      sq_fetch(p);                                   // one block at a time copies host SQEs to the mirror
+      tail = ld_acquire(p.mirrorTail, 0);
+    }
+    for (int k = 0; k < burst && !sh.exiting && sh.qlen < (uint32_t)p.maxColl && sh.cursor < tail; ++k) {
+      // the SQE from the device-memory mirror (L2), 4 independent 16-B loads
+      const uint4* src = reinterpret_cast<const uint4*>(p.sqMirror + (sh.cursor % p.sqDepth));
       uint4 w[4];
-      const char* base = reinterpret_cast<const char*>(slot);
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        asm volatile("ld.relaxed.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(w[q].x), "=r"(w[q].y), "=r"(w[q].z), "=r"(w[q].w) : "l"(base + 16 * q) : "memory");
+      for (int q = 0; q < 4; ++q) w[q] = ld_cg(src + q);
       Sqe e;
       memcpy(&e, w, sizeof(Sqe));
       ++sh.cursor;
-      p.blk[b].sqCursor = sh.cursor;
-      fence_sys();                                   // SQE reads complete before the slot is freed
-      st_volatile_u64(&p.sqCursorHost[b], sh.cursor);
+      // release: the mirror slot's loads are done before the fetcher may reuse it
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(&p.blk[b].sqCursor), "l"(sh.cursor) : "memory");
       sh.lastFetch = now;
       fetched = true;
       if (e.kind == kExit) {
@@ -598,12 +641,6 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
   return cmd;
 }
 
-__device__ __forceinline__ uint64_t ld_acquire(const void* p, int sys) {
-  uint64_t v;
-  if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  else     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 
 // Cursor of one collective on one block: (loop, step, slice) + connector counts.
 struct Cursor {

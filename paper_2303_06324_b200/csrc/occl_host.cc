@@ -104,6 +104,8 @@ struct occlComm {
   char* arena = nullptr;
   size_t dataBytes = 0, flagsBytes = 0;
   CtxSlot* ctx = nullptr;
+  Sqe* sqMirror = nullptr;                       // device copy of the SQ (+ tail, fetch lock)
+  uint64_t* mirrorTail = nullptr;
   BlockState* blk = nullptr;
   uint32_t* tqSave = nullptr;
   uint32_t* complCnt = nullptr;
@@ -166,13 +168,10 @@ occlResult_t cuda_fail(occlComm* c, cudaError_t e) {
     if (e_ != cudaSuccess) return cuda_fail(comm, e_); \
   } while (0)
 
+// SQ slots below this index were copied into the daemon's device-memory mirror
+// (the fetching block publishes it) and may be rewritten.
 uint64_t min_cursor(occlComm* c) {
-  uint64_t m = UINT64_MAX;
-  for (int b = 0; b < c->cfg.gridBlocks; ++b) {
-    uint64_t v = reinterpret_cast<volatile uint64_t*>(c->sqCurHost)[b];
-    if (v < m) m = v;
-  }
-  return m;
+  return reinterpret_cast<volatile uint64_t*>(c->sqCurHost)[0];
 }
 
 bool comm_sticky(occlComm* c) { return c->sticky.load() || (c->L && c->L->sticky.load()); }
@@ -430,6 +429,8 @@ void free_comm(occlComm* c) {
   if (c->ringsDev) cudaFree(c->ringsDev);
   if (c->arena) cudaFree(c->arena);
   if (c->ctx) cudaFree(c->ctx);
+  if (c->sqMirror) cudaFree(c->sqMirror);
+  if (c->mirrorTail) cudaFree(c->mirrorTail);
   if (c->blk) cudaFree(c->blk);
   if (c->tqSave) cudaFree(c->tqSave);
   if (c->complCnt) cudaFree(c->complCnt);
@@ -538,6 +539,9 @@ occlResult_t occlCommCreate(occlComm_t* out, int nranks, int rank, int cudaDev, 
   if ((e = cudaMemset(cp->arena + c->dataBytes, 0, c->flagsBytes)) != cudaSuccess) return fail(e);
   if ((e = cudaMalloc(&cp->ctx, M * G * sizeof(CtxSlot))) != cudaSuccess) return fail(e);
   if ((e = cudaMemset(cp->ctx, 0, M * G * sizeof(CtxSlot))) != cudaSuccess) return fail(e);
+  if ((e = cudaMalloc(&cp->sqMirror, cfg.sqDepth * sizeof(Sqe))) != cudaSuccess) return fail(e);
+  if ((e = cudaMalloc(&cp->mirrorTail, 2 * sizeof(uint64_t))) != cudaSuccess) return fail(e);   // tail, lock
+  if ((e = cudaMemset(cp->mirrorTail, 0, 2 * sizeof(uint64_t))) != cudaSuccess) return fail(e);
   if ((e = cudaMalloc(&cp->blk, G * sizeof(BlockState))) != cudaSuccess) return fail(e);
   if ((e = cudaMemset(cp->blk, 0, G * sizeof(BlockState))) != cudaSuccess) return fail(e);
   if ((e = cudaMalloc(&cp->tqSave, G * M * sizeof(uint32_t))) != cudaSuccess) return fail(e);
@@ -664,6 +668,9 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   DaemonParams& p = c->params;
   p.sq = c->sqDev;
   p.sqCursorHost = c->sqCurDev;
+  p.sqMirror = c->sqMirror;
+  p.mirrorTail = c->mirrorTail;
+  p.fetchLock = reinterpret_cast<uint32_t*>(c->mirrorTail + 1);
   p.cqDone = c->cqDev;
   p.blk = c->blk;
   p.tqSave = c->tqSave;

@@ -127,7 +127,10 @@ struct alignas(16) TraceRec {
 
 struct DaemonParams {
   const Sqe* sq;                    // mapped host SQ
-  volatile uint64_t* sqCursorHost;  // mapped host [G]
+  volatile uint64_t* sqCursorHost;  // mapped host [G]: [0] = SQEs copied to the mirror (slots below are free)
+  Sqe* sqMirror;                    // device [sqDepth]: copy of the host SQ read by every block
+  uint64_t* mirrorTail;             // device: SQEs in the mirror
+  uint32_t* fetchLock;              // device: the block copying host SQEs holds it
   volatile uint64_t* cqDone;        // mapped host [maxColl]: last completed subSeq
   BlockState* blk;                  // [G]
   uint32_t* tqSave;                 // [G][maxColl] packed (id | stall << 16)

@@ -15,7 +15,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libocclb200.so")
+LIB_PATH = os.environ.get("OCCL_LIB_PATH") or os.path.join(_HERE, "lib", "libocclb200.so")
 GEN_PATH = os.path.join(_HERE, "lib", "libocclgen.so")
 
 # ---------------------------------------------------------------- enums (occl.h)
@@ -124,7 +124,11 @@ def _lib():
             "occlTraceReset": [vp],
             "occlCommSplit": [vp, i, C.POINTER(i), C.POINTER(vp)],
         }.items():
-            f = getattr(L, name)
+            f = getattr(L, name, None)
+            if f is None:
+                if os.environ.get("OCCL_LIB_PATH"):
+                    continue                     # diagnostics against an older build
+                raise ImportError(f"{LIB_PATH}: missing symbol {name}")
             f.restype = C.c_int
             f.argtypes = args
         _LIB = L

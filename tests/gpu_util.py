@@ -63,7 +63,10 @@ def make_bufs(kind, dtype, n, count, seed, coll, device=0, inplace=False):
                 if dtype != "bf16" else torch.zeros(out_len(kind, n, count), dtype=torch.bfloat16, device=device)
             sends.append(s)
             recvs.append(rv)
-    torch.cuda.synchronize()
+    # inputs complete before submission (occl.h conventions): sync torch's stream
+    # only -- a device-wide sync would wait for a running persistent daemon
+    # (Fig. 1(c); it returns only once the daemon quits voluntarily)
+    torch.cuda.current_stream(device).synchronize()
     return sends, recvs
 
 
