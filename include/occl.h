@@ -103,6 +103,8 @@ typedef struct {
   int stagingTiles;       /* TMA staging ring depth per block (1..6), 32 KiB of shared memory each */
   int blocksPerSM;        /* 1 (up to 640 threads) or 2 (up to 384 threads, <= 3 staging tiles)    */
   uint32_t traceCap;      /* device event-trace records kept per block (0 = tracing off)          */
+  uint32_t llSliceBytes;  /* LL protocol: payload bytes per slice (multiple of 8; lines are 16 B) */
+  uint32_t llMaxBytes;    /* a collective whose per-block part is <= this uses LL (0 = never)   */
 } occlConfig_t;
 
 /* Aggregate counters (device counters summed over blocks/collectives). */
@@ -149,7 +151,7 @@ typedef struct {
   uint32_t arg;
 } occlTraceRec_t;
 enum { occlEvFetch = 1, occlEvSwitchIn = 2, occlEvIssue = 3, occlEvPublish = 4, occlEvPreempt = 5,
-       occlEvDone = 6, occlEvCqe = 7, occlEvQuit = 8, occlEvExit = 9, occlEvSdone = 10 };
+       occlEvDone = 6, occlEvCqe = 7, occlEvQuit = 8, occlEvExit = 9, occlEvSdone = 10, occlEvStart = 11, occlEvMark = 12 };
 
 /* Bootstrap all-gather: gather `bytesPerRank` bytes from every rank into `out`
  * (rank-major).  Return 0 on success. */

@@ -129,7 +129,8 @@ template <> __device__ __forceinline__ uint4 vadd<kBF16>(const uint4& a, const u
 // Action bits of the fused primitives.
 enum : int { A_RECV = 1, A_REDUCE = 2, A_COPY = 4, A_SEND = 8,
              A_DIN = 16,    // direct receive: the upstream wrote the data into our recv buffer
-             A_DOUT = 32 }; // direct send: write into the downstream's recv buffer, not its connector
+             A_DOUT = 32,   // direct send: write into the downstream's recv buffer, not its connector
+             A_LL = 64 };   // LL protocol: 16-B lines {data, flag, data, flag}, no release fence
 enum : int {
   P_SEND = A_SEND,
   P_RECV = A_RECV | A_COPY,
@@ -412,8 +413,16 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched
   }
   uint64_t part = (segLen + e.nblocks - 1) / e.nblocks;
   part = (part + A - 1) / A * A;
-  const uint64_t E = p.sliceBytes / isz;
-  const uint64_t chunk = E * p.slicesPerChunk;
+  // LL for collectives whose per-block part is small (latency-bound): identical
+  // decision on every rank (same count, ring size, grid size and config)
+  const uint32_t ll = (p.llMaxBytes && n > 1 && part * isz <= p.llMaxBytes) ? 1u : 0u;
+  const uint64_t E = (ll ? p.llSliceBytes : p.sliceBytes) / isz;
+  // a block whose part fits in fewer slices than a chunk sends no empty slices:
+  // every message of the ring is a hop of latency (same on all ranks)
+  uint64_t spc = (part + E - 1) / E;
+  if (spc < 1) spc = 1;
+  if (spc > (uint64_t)p.slicesPerChunk) spc = p.slicesPerChunk;
+  const uint64_t chunk = E * spc;
   uint64_t nloops = (part + chunk - 1) / chunk;
   if (nloops == 0) nloops = 1;
   int nsteps = 1;
@@ -429,10 +438,12 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched
   ns->root = e.root; ns->nblocks = e.nblocks; ns->nsteps = (uint16_t)nsteps; ns->priority = e.priority;
   ns->lane = (uint32_t)lane;
   ns->sub = e.sub;
+  ns->proto = ll;
+  ns->spc = (uint32_t)spc;
   uint4* dst = reinterpret_cast<uint4*>(g);
 #pragma unroll
   for (int i = 0; i < kCtxBytes / 16; ++i) st_cg_v4(dst + i, w[i]);
-  if (R.directPrev && n > 1 && e.kind != kReduceScatter) {
+  if (R.directPrev && n > 1 && e.kind != kReduceScatter && !ll) {
     // tell the upstream where this submission's final data goes (direct mode)
     char* f = R.flagsPrev + ((size_t)c * G + b) * kFlagStride + kDirectOff;
     st_relaxed(f, e.recvbuff, p.sysScope);
@@ -469,34 +480,72 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched
 // still needs the slot it overwrites), publishes the mirror tail, and tells the
 // host which SQ slots are free.  The other blocks read the mirror from L2.  This
 // replaces G PCIe reads per SQE (and per idle poll) with one.
-__device__ __noinline__ void sq_fetch(const DaemonParams& p) {
+__device__ __noinline__ void sq_fetch(const DaemonParams& p, const Smem& m, int b) {
   if (atomicCAS(p.fetchLock, 0u, 1u) != 0u) return;            // another block is fetching
+  trace_at(p, *m.tr, b, kEvMark, 0, 1);
   uint64_t t = ld_relaxed(p.mirrorTail, 0);
-  uint64_t minCur = ~0ull;
-  for (int bb = 0; bb < p.G; ++bb) {
-    uint64_t c;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(c) : "l"(&p.blk[bb].sqCursor) : "memory");
-    minCur = c < minCur ? c : minCur;
+  // the slowest block's cursor bounds which mirror slots may be overwritten; a
+  // cached value is a safe lower bound (cursors only grow), so the G cursors are
+  // re-read only when the mirror looks full -- in parallel, then one fence
+  uint64_t minCur = ld_relaxed(p.mirrorTail + 2, 0);
+  if (t - minCur >= p.sqDepth - 64) {
+    uint64_t m = ~0ull;
+    for (int bb = 0; bb < p.G; ++bb) {
+      const uint64_t c = ld_relaxed(&p.blk[bb].sqCursor, 0);
+      m = c < m ? c : m;
+    }
+    fence_acq_rel(0);                                          // acquire: slot reuse after their loads
+    minCur = m;
+    st_relaxed(p.mirrorTail + 2, m, 0);
   }
   const uint64_t t0 = t;
-  while (t - minCur < p.sqDepth && t - t0 < 64) {
-    const Sqe* slot = p.sq + (t % p.sqDepth);
-    if (ld_acquire_sys(&slot->seq) != t + 1) break;            // written last by the host (release)
-    uint4 w[4];
-    const char* base = reinterpret_cast<const char*>(slot);
+  constexpr int B = 4;
+  for (;;) {
+    // one PCIe round trip: the sequence numbers of up to B slots, read in parallel
+    uint64_t room = p.sqDepth - (t - minCur);
+    if (room > 64 - (t - t0)) room = 64 - (t - t0);
+    const int nb = room < (uint64_t)B ? (int)room : B;
+    if (nb <= 0) break;
+    uint64_t seqs[B];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      asm volatile("ld.relaxed.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(w[q].x), "=r"(w[q].y), "=r"(w[q].z), "=r"(w[q].w) : "l"(base + 16 * q) : "memory");
-    uint4* dst = reinterpret_cast<uint4*>(p.sqMirror + (t % p.sqDepth));
+    for (int i = 0; i < B; ++i)
+      if (i < nb) seqs[i] = ld_relaxed(&p.sq[(t + i) % p.sqDepth].seq, 1);
+    int valid = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) st_cg_v4(dst + q, w[q]);
-    ++t;
+    for (int i = 0; i < B; ++i)
+      if (valid == i && i < nb && seqs[i] == t + i + 1) valid = i + 1;   // seq is written last by the host
+    trace_at(p, *m.tr, b, kEvMark, valid, 2);
+    if (!valid) break;
+    fence_sys();                                               // acquire: the payload loads come after
+    trace_at(p, *m.tr, b, kEvMark, valid, 3);
+    // a second round trip: every valid SQE's payload (4 independent 16-B loads each)
+    uint4 w[B][4];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      if (i >= valid) break;
+      const char* base = reinterpret_cast<const char*>(p.sq + (t + i) % p.sqDepth);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        asm volatile("ld.relaxed.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(w[i][q].x), "=r"(w[i][q].y), "=r"(w[i][q].z), "=r"(w[i][q].w) : "l"(base + 16 * q)
+                     : "memory");
+    }
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      if (i >= valid) break;
+      uint4* dst = reinterpret_cast<uint4*>(p.sqMirror + (t + i) % p.sqDepth);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) st_cg_v4(dst + q, w[i][q]);
+    }
+    t += valid;
+    trace_at(p, *m.tr, b, kEvMark, valid, 4);
+    if (valid < nb) break;
   }
   if (t != t0) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(p.mirrorTail), "l"(t) : "memory");
     fence_sys();                                               // host SQE reads done before the slots are freed
     st_volatile_u64(&p.sqCursorHost[0], t);
+    trace_at(p, *m.tr, b, kEvMark, 0, 5);
   }
   asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p.fetchLock), "r"(0u) : "memory");
 }
@@ -563,7 +612,7 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
     bool fetched = false;
     uint64_t tail = ld_acquire(p.mirrorTail, 0);
     if (tail <= sh.cursor) {
-      sq_fetch(p);                                   // one block at a time copies host SQEs to the mirror
+      sq_fetch(p, m, b);                             // one block at a time copies host SQEs to the mirror
       tail = ld_acquire(p.mirrorTail, 0);
     }
     for (int k = 0; k < burst && !sh.exiting && sh.qlen < (uint32_t)p.maxColl && sh.cursor < tail; ++k) {
@@ -672,7 +721,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   const uint32_t D = (uint32_t)p.pipeDepth;
   CtxSlot& cx = m.cache[sh.way];
   const RingDesc& R = p.rings[cx.sub];                   // the collective's own ring
-  const int n = R.nranks, r = R.rank, K = p.K, sys = p.sysScope, spc = p.slicesPerChunk;
+  const int n = R.nranks, r = R.rank, K = p.K, sys = p.sysScope, spc = (int)cx.spc;
   // ---- static context -> registers
   const uint64_t sendbuff = cx.s.sendbuff, recvbuff = cx.s.recvbuff, count = cx.s.count;
   const uint64_t segLen = cx.s.segLen, part = cx.s.part;
@@ -680,8 +729,12 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   const uint32_t nloops = cx.d.nloops;
   const bool inplace = sendbuff == recvbuff;
   const int isz = elem_size(dtype);
-  const uint64_t E = p.sliceBytes / isz;
+  const bool ll = cx.proto != 0;
+  const uint64_t E = (ll ? p.llSliceBytes : p.sliceBytes) / isz;
   const size_t cb = (size_t)sh.curId * p.G + b;
+  const uint64_t llSlot = 2ull * p.llSliceBytes;                  // bytes of one LL slot (16-B lines)
+  const char* llIn = p.llLocal + cb * K * llSlot;
+  char* llOut = R.llNext + cb * K * llSlot;
   const char* headIn = p.flagsLocal + cb * kFlagStride;
   const char* creditIn = headIn + 128;
   char* headOut = R.flagsNext + cb * kFlagStride;
@@ -689,10 +742,11 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   char* connIn = p.dataLocal + cb * K * p.sliceBytes;
   char* connOut = R.dataNext + cb * K * p.sliceBytes;
   const char* directIn = p.flagsLocal + cb * kFlagStride + kDirectOff;   // {peer recvbuff, subSeq}
-  const bool dOut = R.directNext != 0, dIn = R.directPrev != 0;
+  const bool dOut = R.directNext != 0 && !ll, dIn = R.directPrev != 0 && !ll;
   const uint64_t subSeq = cx.s.subSeq;
   uint64_t peerRecv = 0;                                  // downstream's recv buffer (direct sends)
   bool prepared = false;                                  // pipe.ring[issued % D] holds the next slice
+  const char* llLast = nullptr;                           // LL: last line of the next slice's input
   int curPrim = 0;
   uint64_t doutOff = 0;
   // ---- dynamic context -> registers
@@ -743,9 +797,18 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
       doutOff = (recvOff + lo) * isz;
       sd.src = reinterpret_cast<const char*>(sendbuff) + (sendOff + lo) * isz;
       sd.dst = reinterpret_cast<char*>(recvbuff) + doutOff;
-      sd.cin = (curPrim & A_DIN) ? sd.dst : connIn + (di.nrecv % K) * p.sliceBytes;
-      sd.cout = connOut + (di.nsent % K) * p.sliceBytes;   // direct sends: set once the peer is known
       sd.nelem = hi > lo ? (int64_t)(hi - lo) : 0;
+      if (ll) {
+        curPrim |= A_LL;
+        sd.cin = llIn + (di.nrecv % K) * llSlot;
+        sd.cout = llOut + (di.nsent % K) * llSlot;
+        // the receiver polls the slice's last line (every message has >= 1 line)
+        const uint64_t lines = ((uint64_t)sd.nelem * isz + 7) / 8;
+        llLast = sd.cin + 16 * ((lines ? lines : 1) - 1);
+      } else {
+        sd.cin = (curPrim & A_DIN) ? sd.dst : connIn + (di.nrecv % K) * p.sliceBytes;
+        sd.cout = connOut + (di.nsent % K) * p.sliceBytes;   // direct sends: set once the peer is known
+      }
       sd.prim = curPrim;
       sd.dtype = dtype;
       sd.headOut = headOut;
@@ -759,7 +822,14 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     const bool needRecv = prim & A_RECV, needSend = prim & A_SEND;
     bool ok = true;
     const long long tp = clock64();
-    if (needRecv && di.nrecv >= headSeen) {
+    if (needRecv && (prim & A_LL)) {
+      // LL: the data carries its own flags -- the last line of the slice holds
+      // the message sequence number once the upstream wrote it
+      uint32_t f0, f1;
+      asm volatile("{\n .reg .u32 a, c;\n ld.volatile.global.v4.u32 {a, %0, c, %1}, [%2];\n}"
+                   : "=r"(f0), "=r"(f1) : "l"(llLast) : "memory");
+      ok = f0 == (uint32_t)(di.nrecv + 1) && f1 == (uint32_t)(di.nrecv + 1);
+    } else if (needRecv && di.nrecv >= headSeen) {
       headSeen = ld_acquire(headIn, sys);
       ok = di.nrecv < headSeen;
     }
@@ -842,6 +912,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
 __device__ __noinline__ void control_main(const DaemonParams& p, int b, Sched& sh, const Smem& m, Pipe& pipe) {
   const uint32_t D = (uint32_t)p.pipeDepth;
   uint32_t issued = 0, committed = 0;               // kernel-lifetime slice counters
+  trace_at(p, *m.tr, b, kEvStart, 0, (uint32_t)sh.cursor);
   for (;;) {
     const int cmd = schedule(p, b, sh, m);
     if (cmd == CMD_NONE) continue;
@@ -929,6 +1000,7 @@ __device__ __noinline__ void producer_main(const DaemonParams& p, Pipe& pipe, St
     const SliceDesc sd = pipe.ring[j % D];
     if (sd.prim == P_EXIT) break;
     if (!(sd.prim & (A_COPY | A_SEND))) continue;     // direct final receive: data already in place
+    if (sd.prim & A_LL) continue;                     // LL slices are moved by the compute warps alone
     const int vb = tma_vec_bytes(sd.dtype, sd.nelem, sd.src, sd.dst, sd.cout);
     if (vb == 0) continue;
     // order the acquire of the peer's head (generic proxy) before the bulk reads (async proxy)
@@ -971,6 +1043,56 @@ __device__ __forceinline__ void consume_tile(const int prim, char* dst, char* co
   }
 }
 
+// LL slice (NCCL's low-latency protocol idea, re-done for the daemon): every
+// 16-B line carries 8 B of payload and the message sequence number twice,
+// written with one 16-B store, so the receiver needs no head flag and the
+// sender no release fence -- a line is valid once both flags match.  Used for
+// latency-bound collectives (small per-block parts).  Payload = the slice's
+// elements packed 8 B per line; reduction per element as in the Simple path.
+template <int DT>
+__device__ __forceinline__ void ll_slice(const int prim, const char* src, const char* cin, char* dst, char* cout,
+                                         const int64_t nelem, const uint32_t inSeq, const uint32_t outSeq,
+                                         const int tid, const int nt) {
+  typedef typename Elem<DT>::T T;
+  constexpr int PER = 8 / sizeof(T);                 // elements per line
+  const bool recv = prim & A_RECV, reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
+  const int64_t lines = (nelem + PER - 1) / PER;
+  const int64_t nl = lines ? lines : 1;              // an empty message still carries one token line
+  const T* s = reinterpret_cast<const T*>(src);
+  T* d = reinterpret_cast<T*>(dst);
+  for (int64_t l = tid; l < nl; l += nt) {
+    union { uint32_t w[2]; T e[PER]; } pay;
+    pay.w[0] = pay.w[1] = 0;
+    const int64_t e0 = l * PER;
+    if (recv) {
+      uint32_t x0, f0, x1, f1;
+      do {
+        asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(x0), "=r"(f0), "=r"(x1), "=r"(f1) : "l"(cin + 16 * l) : "memory");
+      } while (f0 != inSeq || f1 != inSeq);
+      pay.w[0] = x0;
+      pay.w[1] = x1;
+      if (reduce) {
+#pragma unroll
+        for (int k = 0; k < PER; ++k)
+          if (e0 + k < nelem) pay.e[k] = sadd<DT>(pay.e[k], __ldcg(s + e0 + k));
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < PER; ++k)
+        if (e0 + k < nelem) pay.e[k] = __ldcg(s + e0 + k);
+    }
+    if (copy) {
+#pragma unroll
+      for (int k = 0; k < PER; ++k)
+        if (e0 + k < nelem) d[e0 + k] = pay.e[k];
+    }
+    if (send)
+      asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};"
+                   :: "l"(cout + 16 * l), "r"(pay.w[0]), "r"(outSeq), "r"(pay.w[1]), "r"(outSeq) : "memory");
+  }
+}
+
 // Compute warps: every compute warp takes part in every slice, in order.  The
 // descriptor is read field by field into registers (a struct copy would live in
 // local memory and be re-read in the inner loop).
@@ -998,7 +1120,12 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
     char* cout = dp->cout;
     const long long t1 = clock64();
     const int vb = tma_vec_bytes(dtype, nelem, src, dst, cout);
-    if (!(prim & (A_COPY | A_SEND))) {
+    if (prim & A_LL) {
+      const uint32_t inSeq = (uint32_t)dp->creditVal, outSeq = (uint32_t)dp->headVal;
+      if (dtype == kBF16) ll_slice<kBF16>(prim, src, cin, dst, cout, nelem, inSeq, outSeq, ctid, cnt);
+      else if (dtype == kF32) ll_slice<kF32>(prim, src, cin, dst, cout, nelem, inSeq, outSeq, ctid, cnt);
+      else ll_slice<kI32>(prim, src, cin, dst, cout, nelem, inSeq, outSeq, ctid, cnt);
+    } else if (!(prim & (A_COPY | A_SEND))) {
       // direct final receive: the data is already in place, nothing to move
     } else if (vb == 0) {                              // small or misaligned: register path
       if (dtype == kBF16) move_slice<kBF16>(prim, src, cin, dst, cout, nelem, ctid, cnt);
@@ -1078,7 +1205,7 @@ __device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& 
       break;
     }
     mbar_wait(&pipe.sdone[i], (j / D) & 1);
-    bool send = false, recv = false;
+    bool send = false, recv = false, needFence = false;
     uint64_t hv = 0, cv = 0;
     char* ho = nullptr;
     char* co = nullptr;
@@ -1087,6 +1214,9 @@ __device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& 
       const SliceDesc& d = pipe.ring[k % D];
       if (d.prim & A_SEND) { send = true; hv = d.headVal; ho = d.headOut; }
       if (d.prim & A_RECV) { recv = true; cv = d.creditVal; co = d.creditOut; }
+      // LL data needs no release (its lines carry their own flags); LL credits
+      // follow loads that already returned their values
+      if ((d.prim & (A_SEND | A_RECV)) && !(d.prim & A_LL)) needFence = true;
       const uint32_t k1 = k + 1;
       if (!mbar_test(&pipe.full[k1 % D], (k1 / D) & 1)) break;
       const SliceDesc& d1 = pipe.ring[k1 % D];
@@ -1097,7 +1227,7 @@ __device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& 
       k = k1;
     }
     trace_at(p, pipe.tr, b, kEvSdone, k - j + 1, (uint32_t)(hv & 0xffff) | ((uint32_t)(cv & 0xffff) << 16));
-    if (send || recv) fence_acq_rel(sys);
+    if (needFence) fence_acq_rel(sys);
     if (send) red_max_relaxed(ho, hv, sys);     // head of rank r+1
     if (recv) red_max_relaxed(co, cv, sys);     // credit of rank r-1
     trace_at(p, pipe.tr, b, kEvPublish, k - j + 1, (uint32_t)(hv & 0xffff) | ((uint32_t)(cv & 0xffff) << 16));

@@ -34,14 +34,14 @@ using namespace occl;
 namespace {
 
 constexpr uint32_t kHandleMagic = 0x4f43434cu;   // "OCCL"
-constexpr uint32_t kHandleVersion = 1;
+constexpr uint32_t kHandleVersion = 2;
 
 struct Handle {
   uint32_t magic, version;
   int32_t nranks, rank, dev, pid;
   uint64_t hostId;
   uint64_t arenaPtr;
-  uint64_t dataBytes, flagsOffset;
+  uint64_t dataBytes, flagsOffset, llOffset;
   uint64_t cfgFingerprint;
   cudaIpcMemHandle_t ipc;
 };
@@ -66,6 +66,8 @@ uint64_t fingerprint(const occlConfig_t& c) {
   mix(c.maxColl); mix(c.gridBlocks); mix(c.connSlots); mix(c.slicesPerChunk); mix(c.sliceBytes);
   mix(c.minBlockBytes);
   mix(c.directMode);
+  mix(c.llSliceBytes);
+  mix(c.llMaxBytes);
   return h;
 }
 
@@ -102,7 +104,7 @@ struct occlComm {
   occlConfig_t cfg{};
   // device memory
   char* arena = nullptr;
-  size_t dataBytes = 0, flagsBytes = 0;
+  size_t dataBytes = 0, flagsBytes = 0, llBytes = 0;
   CtxSlot* ctx = nullptr;
   Sqe* sqMirror = nullptr;                       // device copy of the SQ (+ tail, fetch lock)
   uint64_t* mirrorTail = nullptr;
@@ -331,6 +333,7 @@ occlResult_t validate_config(const occlConfig_t& c) {
   if (c.stagingTiles < 1 || c.stagingTiles > 6) return occlInvalidArgument;
   if (c.blocksPerSM < 1 || c.blocksPerSM > 2) return occlInvalidArgument;
   if (c.traceCap > (1u << 24)) return occlInvalidArgument;
+  if (c.llSliceBytes < 8 || c.llSliceBytes % 8 || c.llSliceBytes > (1u << 20)) return occlInvalidArgument;
   if (c.blocksPerSM == 2 && (c.blockThreads > 384 || c.stagingTiles > 3)) return occlInvalidArgument;
   return occlSuccess;
 }
@@ -502,6 +505,8 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->discardConsumed = 1;
   c->directMode = 1;
   c->stagingTiles = 6;
+  c->llSliceBytes = 8 << 10;
+  c->llMaxBytes = 64 << 10;
   c->blocksPerSM = 1;
   c->l2Hints = 1;
   return occlSuccess;
@@ -524,6 +529,7 @@ occlResult_t occlCommCreate(occlComm_t* out, int nranks, int rank, int cudaDev, 
   const size_t M = cfg.maxColl, G = cfg.gridBlocks;
   c->dataBytes = M * G * cfg.connSlots * cfg.sliceBytes;
   c->flagsBytes = M * G * kFlagStride;
+  c->llBytes = M * G * cfg.connSlots * 2ull * cfg.llSliceBytes;
   c->subSeq.assign(M, 0);
   c->state.reset(new std::atomic<int>[M]);
   for (size_t i = 0; i < M; ++i) c->state[i].store(0);
@@ -535,13 +541,15 @@ occlResult_t occlCommCreate(occlComm_t* out, int nranks, int rank, int cudaDev, 
   auto fail = [&](cudaError_t) { free_comm(cp); return occlCudaError; };
   cudaError_t e;
   if ((e = cudaSetDevice(cudaDev)) != cudaSuccess) return fail(e);
-  if ((e = cudaMalloc(&cp->arena, c->dataBytes + c->flagsBytes)) != cudaSuccess) return fail(e);
-  if ((e = cudaMemset(cp->arena + c->dataBytes, 0, c->flagsBytes)) != cudaSuccess) return fail(e);
+  if ((e = cudaMalloc(&cp->arena, c->dataBytes + c->flagsBytes + c->llBytes)) != cudaSuccess) return fail(e);
+  // flags and LL lines start at 0: LL flags are message sequence numbers >= 1
+  if ((e = cudaMemset(cp->arena + c->dataBytes, 0, c->flagsBytes + c->llBytes)) != cudaSuccess) return fail(e);
   if ((e = cudaMalloc(&cp->ctx, M * G * sizeof(CtxSlot))) != cudaSuccess) return fail(e);
   if ((e = cudaMemset(cp->ctx, 0, M * G * sizeof(CtxSlot))) != cudaSuccess) return fail(e);
   if ((e = cudaMalloc(&cp->sqMirror, cfg.sqDepth * sizeof(Sqe))) != cudaSuccess) return fail(e);
-  if ((e = cudaMalloc(&cp->mirrorTail, 2 * sizeof(uint64_t))) != cudaSuccess) return fail(e);   // tail, lock
-  if ((e = cudaMemset(cp->mirrorTail, 0, 2 * sizeof(uint64_t))) != cudaSuccess) return fail(e);
+  // tail, fetch lock, cached minimum block cursor
+  if ((e = cudaMalloc(&cp->mirrorTail, 3 * sizeof(uint64_t))) != cudaSuccess) return fail(e);
+  if ((e = cudaMemset(cp->mirrorTail, 0, 3 * sizeof(uint64_t))) != cudaSuccess) return fail(e);
   if ((e = cudaMalloc(&cp->blk, G * sizeof(BlockState))) != cudaSuccess) return fail(e);
   if ((e = cudaMemset(cp->blk, 0, G * sizeof(BlockState))) != cudaSuccess) return fail(e);
   if ((e = cudaMalloc(&cp->tqSave, G * M * sizeof(uint32_t))) != cudaSuccess) return fail(e);
@@ -587,6 +595,7 @@ occlResult_t occlCommGetHandle(occlComm_t c, void* out, size_t* len) {
   h.arenaPtr = (uint64_t)(uintptr_t)c->arena;
   h.dataBytes = c->dataBytes;
   h.flagsOffset = c->dataBytes;
+  h.llOffset = c->dataBytes + c->flagsBytes;
   h.cfgFingerprint = fingerprint(c->cfg);
   cudaSetDevice(c->dev);
   if (cudaIpcGetMemHandle(&h.ipc, c->arena) != cudaSuccess) {
@@ -656,6 +665,7 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   // ring 0: this communicator's own ring
   RingDesc rd{};
   rd.dataNext = c->nextArena;
+  rd.llNext = c->nextArena + hs[next].llOffset;
   rd.flagsNext = c->nextArena + hs[next].flagsOffset;
   rd.flagsPrev = c->prevArena + hs[prev].flagsOffset;
   rd.nranks = c->nranks;
@@ -713,6 +723,9 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   p.directNext = c->cfg.directMode && !c->nextIpc;
   p.directPrev = c->cfg.directMode && !c->prevIpc;
   p.rings = c->ringsDev;
+  p.llLocal = c->arena + c->dataBytes + c->flagsBytes;
+  p.llSliceBytes = c->cfg.llSliceBytes;
+  p.llMaxBytes = c->cfg.llMaxBytes;
   p.trace = c->trace;
   p.traceCount = c->traceCount;
   p.traceCap = c->cfg.traceCap;
@@ -799,6 +812,7 @@ occlResult_t occlCommSplit(occlComm_t parent, int nmembers, const int* members, 
   if ((r = peer(pq, &pa)) != occlSuccess) return r;
   RingDesc rd{};
   rd.dataNext = na;
+  rd.llNext = na + P->handles[nq].llOffset;
   rd.flagsNext = na + P->handles[nq].flagsOffset;
   rd.flagsPrev = pa + P->handles[pq].flagsOffset;
   rd.nranks = nmembers;

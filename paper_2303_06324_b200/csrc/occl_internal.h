@@ -43,6 +43,7 @@ constexpr int kMaxRings = 32;           // communicator + sub-communicators serv
 // (collId, block) in every member's arena, so only the neighbours differ.
 struct alignas(16) RingDesc {
   char* dataNext;      // downstream member's connector data
+  char* llNext;        // downstream member's LL connector lines
   char* flagsNext;     // downstream member's flags
   char* flagsPrev;     // upstream member's flags
   int32_t nranks, rank;
@@ -81,7 +82,9 @@ struct alignas(16) CtxSlot {
   int32_t priority;
   uint32_t lane;       // this block's lane in the collective: (block - collId) mod G
   uint32_t sub;        // ring (RingDesc index) of the collective
-  uint32_t pad[5];
+  uint32_t proto;      // 0 = Simple (TMA slices, head/credit flags), 1 = LL (flags inside the data)
+  uint32_t spc;        // slices per chunk of this collective: min(cfg, slices a block's part needs)
+  uint32_t pad[3];
 };
 static_assert(sizeof(CtxSlot) == kCtxBytes, "CtxSlot must be 128 B");
 
@@ -117,7 +120,7 @@ struct alignas(16) BlockStat {  // per block
 // per-hop latency analysis of the ring.
 enum TraceEv : uint32_t {
   kEvFetch = 1, kEvSwitchIn = 2, kEvIssue = 3, kEvPublish = 4, kEvPreempt = 5, kEvDone = 6, kEvCqe = 7,
-  kEvQuit = 8, kEvExit = 9, kEvSdone = 10
+  kEvQuit = 8, kEvExit = 9, kEvSdone = 10, kEvStart = 11, kEvMark = 12
 };
 struct alignas(16) TraceRec {
   uint64_t t;          // %globaltimer (ns)
@@ -129,7 +132,7 @@ struct DaemonParams {
   const Sqe* sq;                    // mapped host SQ
   volatile uint64_t* sqCursorHost;  // mapped host [G]: [0] = SQEs copied to the mirror (slots below are free)
   Sqe* sqMirror;                    // device [sqDepth]: copy of the host SQ read by every block
-  uint64_t* mirrorTail;             // device: SQEs in the mirror
+  uint64_t* mirrorTail;             // device: [0] SQEs in the mirror, [1] fetch lock, [2] cached min block cursor
   uint32_t* fetchLock;              // device: the block copying host SQEs holds it
   volatile uint64_t* cqDone;        // mapped host [maxColl]: last completed subSeq
   BlockState* blk;                  // [G]
@@ -162,6 +165,9 @@ struct DaemonParams {
   TraceRec* trace;                  // [G][traceCap] or null
   uint32_t* traceCount;             // [G] records written (monotonic; ring index = count % traceCap)
   uint32_t traceCap;
+  char* llLocal;                    // this rank's LL connector lines [maxColl][G][K][2 * llSliceBytes]
+  uint32_t llSliceBytes;            // LL payload per slice (lines carry 8 B payload + 8 B flags)
+  uint32_t llMaxBytes;              // a collective uses LL when its per-block part is at most this
   int stages;                       // TMA staging tiles per block (x 2 x 16 KiB of shared memory)
   int blocksPerSM;                  // 1 or 2 co-resident daemon blocks per SM
   int l2Hints;                      // evict-first L2 policy for user-buffer loads / stores

@@ -38,7 +38,7 @@ EXPORTED = [
     "occlCommSplit",
 ]
 TRACE_EVENTS = {1: "fetch", 2: "switch_in", 3: "issue", 4: "publish", 5: "preempt", 6: "done", 7: "cqe",
-                8: "quit", 9: "exit", 10: "sdone"}
+                8: "quit", 9: "exit", 10: "sdone", 11: "start", 12: "mark"}
 
 
 class occlConfig_t(C.Structure):
@@ -51,6 +51,7 @@ class occlConfig_t(C.Structure):
         ("quitIdleNs", C.c_uint64), ("idleSleepNs", C.c_uint32), ("autoLaunch", C.c_int), ("cacheWays", C.c_int),
         ("pipeDepth", C.c_int), ("prefetchSlices", C.c_int), ("discardConsumed", C.c_int), ("l2Hints", C.c_int),
         ("directMode", C.c_int), ("stagingTiles", C.c_int), ("blocksPerSM", C.c_int), ("traceCap", C.c_uint32),
+        ("llSliceBytes", C.c_uint32), ("llMaxBytes", C.c_uint32),
     ]
 
 
