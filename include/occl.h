@@ -105,6 +105,7 @@ typedef struct {
   uint32_t traceCap;      /* device event-trace records kept per block (0 = tracing off)          */
   uint32_t llSliceBytes;  /* LL protocol: payload bytes per slice (multiple of 8; lines are 16 B) */
   uint32_t llMaxBytes;    /* a collective whose per-block part is <= this uses LL (0 = never)   */
+  uint32_t spinNs;        /* one spin = this many ns of failed polling (thresholds are in spins)  */
 } occlConfig_t;
 
 /* Aggregate counters (device counters summed over blocks/collectives). */

@@ -480,8 +480,8 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched
 // still needs the slot it overwrites), publishes the mirror tail, and tells the
 // host which SQ slots are free.  The other blocks read the mirror from L2.  This
 // replaces G PCIe reads per SQE (and per idle poll) with one.
-__device__ __noinline__ void sq_fetch(const DaemonParams& p, const Smem& m, int b) {
-  if (atomicCAS(p.fetchLock, 0u, 1u) != 0u) return;            // another block is fetching
+__device__ __noinline__ bool sq_fetch(const DaemonParams& p, const Smem& m, int b) {
+  if (atomicCAS(p.fetchLock, 0u, 1u) != 0u) return true;       // another block is fetching
   trace_at(p, *m.tr, b, kEvMark, 0, 1);
   uint64_t t = ld_relaxed(p.mirrorTail, 0);
   // the slowest block's cursor bounds which mirror slots may be overwritten; a
@@ -499,12 +499,12 @@ __device__ __noinline__ void sq_fetch(const DaemonParams& p, const Smem& m, int 
     st_relaxed(p.mirrorTail + 2, m, 0);
   }
   const uint64_t t0 = t;
-  constexpr int B = 4;
+  constexpr int B = 8;
   for (;;) {
     // one PCIe round trip: the sequence numbers of up to B slots, read in parallel
     uint64_t room = p.sqDepth - (t - minCur);
-    if (room > 64 - (t - t0)) room = 64 - (t - t0);
-    const int nb = room < (uint64_t)B ? (int)room : B;
+    if (room > 256 - (t - t0)) room = 256 - (t - t0);
+    const int nb = room < (uint64_t)B ? (int)room : B;   // (at most 256 SQEs per call)
     if (nb <= 0) break;
     uint64_t seqs[B];
 #pragma unroll
@@ -548,6 +548,7 @@ __device__ __noinline__ void sq_fetch(const DaemonParams& p, const Smem& m, int 
     trace_at(p, *m.tr, b, kEvMark, 0, 5);
   }
   asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p.fetchLock), "r"(0u) : "memory");
+  return false;
 }
 
 // One scheduling round: bookkeeping of the previous run, SQ fetch, entry
@@ -756,7 +757,10 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   uint32_t pfAhead = 0;
   const uint64_t laneLo = (uint64_t)cx.lane * part;
   uint64_t headSeen = 0, creditSeen = 0;
-  uint64_t T = sh.T, spins = 0;
+  // spins are counted in time: T x spinNs of failed polling (R1) --
+  // an LL poll (a 16-B line in L2) and a cached head poll differ 10x in cost
+  uint64_t T = sh.T, spinStart = 0;
+  const uint64_t spinNs = p.spinNs;
   unsigned long long nSlices = 0, cPoll = 0, cFence = 0;
   const long long tRun = clock64();
   trace_at(p, *m.tr, b, kEvSwitchIn, sh.curId, sh.pos);
@@ -843,7 +847,9 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     }
     if (!ok) {
       cPoll += clock64() - tp;
-      if (++spins > T) {                                  // two-phase blocking: preempt
+      const uint64_t now = globaltimer();
+      if (spinStart == 0) spinStart = now;
+      if (now - spinStart > T * spinNs) {                // two-phase blocking: preempt
         while (committed != issued) {                    // drain the pipe
           mbar_wait(&pipe.empty[committed % D], (committed / D) & 1);
           advance(dc, pipe.ring[committed % D].prim, spc, nsteps);
@@ -855,7 +861,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
       }
       continue;
     }
-    spins = 0;
+    spinStart = 0;
     if (prim & A_DOUT) sd.cout = reinterpret_cast<char*>(peerRecv) + doutOff;
     mbar_arrive(&pipe.full[issued % D]);
     trace_at(p, *m.tr, b, kEvIssue, sh.curId,

@@ -326,6 +326,7 @@ occlResult_t validate_config(const occlConfig_t& c) {
   if (c.sqDepth < 2) return occlInvalidArgument;
   if (c.cacheWays < 1 || c.cacheWays > kMaxCacheWays) return occlInvalidArgument;
   if (c.spinMin < 1 || c.spinBase < c.spinMin || c.spinCap < c.spinBase || c.spinBoost < 1) return occlInvalidArgument;
+  if (c.spinNs < 1) return occlInvalidArgument;
   if (c.priorityCadence < 1) return occlInvalidArgument;
   if (c.stallLimit < 1) return occlInvalidArgument;
   if (c.pipeDepth < 1 || c.pipeDepth > 8) return occlInvalidArgument;
@@ -494,6 +495,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->spinMin = 128;
   c->spinBoost = 2;
   c->spinCap = 65536;
+  c->spinNs = 40;                         // measured cost of a failed head poll (R1)
   c->stallLimit = 2;
   c->quitEnabled = 1;
   c->quitIdleNs = 1'000'000;
@@ -709,6 +711,7 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   p.spinMin = c->cfg.spinMin;
   p.spinBoost = c->cfg.spinBoost;
   p.spinCap = c->cfg.spinCap;
+  p.spinNs = c->cfg.spinNs;
   p.stallLimit = c->cfg.stallLimit;
   p.quitEnabled = c->cfg.quitEnabled;
   p.quitIdleNs = c->cfg.quitIdleNs;

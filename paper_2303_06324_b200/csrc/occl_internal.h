@@ -151,6 +151,7 @@ struct DaemonParams {
   int nranks, rank, G, maxColl, K, slicesPerChunk;
   int orderPolicy, priorityCadence, stickiness;
   uint32_t spinBase, spinStep, spinMin, spinBoost, spinCap, stallLimit;
+  uint32_t spinNs;                  // duration of one spin (failed poll) in ns
   int quitEnabled;
   uint64_t quitIdleNs;
   uint32_t idleSleepNs;

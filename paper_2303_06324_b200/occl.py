@@ -51,7 +51,7 @@ class occlConfig_t(C.Structure):
         ("quitIdleNs", C.c_uint64), ("idleSleepNs", C.c_uint32), ("autoLaunch", C.c_int), ("cacheWays", C.c_int),
         ("pipeDepth", C.c_int), ("prefetchSlices", C.c_int), ("discardConsumed", C.c_int), ("l2Hints", C.c_int),
         ("directMode", C.c_int), ("stagingTiles", C.c_int), ("blocksPerSM", C.c_int), ("traceCap", C.c_uint32),
-        ("llSliceBytes", C.c_uint32), ("llMaxBytes", C.c_uint32),
+        ("llSliceBytes", C.c_uint32), ("llMaxBytes", C.c_uint32), ("spinNs", C.c_uint32),
     ]
 
 
