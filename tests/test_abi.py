@@ -54,6 +54,17 @@ def test_config_defaults_and_validation():
         occl.occlCommCreate(2, 5, 0, cfg)
     assert e.value.code == occl.occlInvalidArgument
     assert occl.occlGetErrorString(occl.occlDuplicateSubmit) == "collective already in flight"
+    # every validated knob is rejected synchronously, before any CUDA call
+    for kw in (dict(llSliceBytes=12), dict(llSliceBytes=0), dict(spinNs=0), dict(stagingTiles=7),
+               dict(blocksPerSM=3), dict(blocksPerSM=2, blockThreads=608), dict(blockThreads=96),
+               dict(blockThreads=672), dict(pipeDepth=9), dict(spinBase=10, spinMin=20), dict(sliceBytes=100),
+               dict(traceCap=1 << 25)):
+        with pytest.raises(occl.OcclError) as e:
+            occl.occlCommCreate(2, 0, 0, occl.occlConfigDefault(**kw))
+        assert e.value.code == occl.occlInvalidArgument, kw
+    # defaults: LL for small parts, direct mode, time-based spins, tracing off
+    assert cfg.llMaxBytes > 0 and cfg.llSliceBytes % 8 == 0 and cfg.directMode == 1
+    assert cfg.spinNs > 0 and cfg.traceCap == 0 and cfg.blockThreads == 608
 
 
 def test_product_path_never_touches_oracle():
