@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--ranks", type=int, default=8)
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "i32"])
     ap.add_argument("--grid-blocks", type=int, default=18)
-    ap.add_argument("--slice-kib", type=int, default=128)
+    ap.add_argument("--slice-kib", type=int, default=192)
     ap.add_argument("--conn-slots", type=int, default=4)
     ap.add_argument("--slices-per-chunk", type=int, default=2)
     ap.add_argument("--threads", type=int, default=608)
@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--discard", type=int, default=1)
     ap.add_argument("--l2-hints", type=int, default=1)
     ap.add_argument("--direct", type=int, default=1)
-    ap.add_argument("--stages", type=int, default=6)
+    ap.add_argument("--stages", type=int, default=5)
     ap.add_argument("--blocks-per-sm", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -1,5 +1,5 @@
 """GPU parity in the launch configuration bench.py times (SURVEY.md §8(c),
-DESIGN.md §4): 128 KiB slices through the TMA staging ring, publisher lane,
+DESIGN.md §4): 192 KiB slices through a 5-stage TMA staging ring, publisher lane,
 direct mode, L2 discard / evict-first hints -- the data path the headline
 number comes from -- plus its variants and guards.
 
@@ -22,8 +22,8 @@ pytestmark = pytest.mark.gpu
 
 import gpu_util as U  # noqa: E402
 
-BENCH = dict(gridBlocks=18, sliceBytes=128 << 10, connSlots=4, slicesPerChunk=2, blockThreads=608, pipeDepth=4,
-             maxColl=16)
+BENCH = dict(gridBlocks=18, sliceBytes=192 << 10, connSlots=4, slicesPerChunk=2, blockThreads=608, pipeDepth=4,
+             stagingTiles=5, maxColl=16)
 
 
 @pytest.fixture(scope="module")
@@ -70,7 +70,7 @@ def test_bench_config_full_size_sampled(occl_mod):
         seg = -(-seg // 4) * 4                               # owner map: L rounded to 16 B
         part = -(-seg // 18)
         part = -(-part // 4) * 4
-        E = (128 << 10) // 4
+        E = BENCH["sliceBytes"] // 4
         bnd = set()
         for q in range(n):
             for lane in range(18):
