@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "lib")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
-                 "-I" + os.path.join(ROOT, "include"), "-Xptxas", "-v", "-lpthread"]
+                 "-I" + os.path.join(ROOT, "include"), "-Xptxas", "-v", "-maxrregcount=104", "-lpthread"]
 
 TARGETS = {
     "libocclb200.so": ["occl_daemon.cu", "occl_host.cc"],

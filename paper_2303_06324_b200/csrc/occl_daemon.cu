@@ -349,7 +349,7 @@ enum : int { CMD_NONE = 0, CMD_RUN = 1, CMD_EXIT = 2 };
 enum : int { RUN_PREEMPT = 0, RUN_GO = 1, RUN_DONE = 2 };
 constexpr int P_EXIT = 0x100;          // descriptor telling the data warps to leave
 constexpr int kMaxDepth = 8;           // max slices in flight between control and data warps
-constexpr int kMaxBlockThreads = 640;  // control + TMA producer + publisher warps + up to 17 compute warps
+constexpr int kMaxBlockThreads = 608;  // control + TMA producer + publisher warps + up to 16 compute warps (104 registers)
 constexpr int kRoleWarps = 3;          // warps 0..2: control, producer, publisher
 constexpr int kTile = 16384;           // TMA staging tile (bytes per operand)
 constexpr int kMaxStages = 6;          // staging ring depth: up to 6 x 2 x 16 KiB of loads in flight

@@ -319,7 +319,7 @@ void launcher_stop(Launcher* L) {
 occlResult_t validate_config(const occlConfig_t& c) {
   if (c.maxColl < 1 || c.maxColl > 65535) return occlInvalidArgument;
   if (c.gridBlocks < 1 || c.gridBlocks > 1024) return occlInvalidArgument;
-  if (c.blockThreads < 128 || c.blockThreads > 640 || c.blockThreads % 32) return occlInvalidArgument;
+  if (c.blockThreads < 128 || c.blockThreads > 608 || c.blockThreads % 32) return occlInvalidArgument;
   if (c.slicesPerChunk < 1 || c.connSlots <= c.slicesPerChunk) return occlInvalidArgument;  // invariant I7
   if (c.sliceBytes < 16 || c.sliceBytes % 16 || c.sliceBytes > (1ull << 30)) return occlInvalidArgument;
   if (c.minBlockBytes < 1) return occlInvalidArgument;
