@@ -408,7 +408,7 @@ def run_occl(args):
                    "ranks": R, "ranks_per_gpu": V, "size_bytes_per_rank": size, "grid_blocks": args.grid_blocks,
                    "slice_bytes": args.slice_kib * 1024, "conn_slots": args.conn_slots,
                    "slices_per_chunk": args.slices_per_chunk, "block_threads": args.threads,
-                   "pipe_depth": args.pipe_depth, "prefetch_slices": args.prefetch, "l2": "inputs larger than L2 (R x S >> 126 MB)",
+                   "pipe_depth": args.pipe_depth, "staging_tiles": args.stages, "prefetch_slices": args.prefetch, "l2": "inputs larger than L2 (R x S >> 126 MB)",
                    "algbw_GBps": size / (ms_step / 1e3) / 1e9},
         "gpu_launches": launches,
         "clocks": clk.summary(),
