@@ -481,7 +481,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->blockThreads = 608;                 // 3 role warps + 16 compute warps
   c->connSlots = 4;
   c->slicesPerChunk = 2;
-  c->sliceBytes = 128 << 10;
+  c->sliceBytes = 192 << 10;
   c->minBlockBytes = 128 << 10;
   c->sqDepth = 1024;
   c->orderPolicy = occlOrderPriority;   // priority = collId unless set (reading R10)
@@ -506,7 +506,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->prefetchSlices = 0;
   c->discardConsumed = 1;
   c->directMode = 1;
-  c->stagingTiles = 6;
+  c->stagingTiles = 5;
   c->llSliceBytes = 8 << 10;
   c->llMaxBytes = 64 << 10;
   c->blocksPerSM = 1;
