@@ -92,6 +92,8 @@ class CollMeta:
     nblocks: int = 1
     inplace: bool = False
     priority: int | None = None    # priority policy: globally agreed, lower first (default coll_id)
+    members: tuple | None = None   # sub-communicator ring (parent ranks in ring order); None = all
+                                   # (the static context carries nranks / rank)
 
 
 @dataclass
@@ -126,6 +128,7 @@ class _Static:
     sendbuf: np.ndarray
     recvbuf: np.ndarray
     sub_index: int
+    members: tuple = ()            # the collective's ring (parent ranks)
 
 
 class _Connector:
@@ -254,6 +257,11 @@ def lane_geometry(meta: CollMeta, n: int, rank: int, cfg: SimConfig):
     chunk = cfg.slices_per_chunk * cfg.slice_elems
     nloops = max(1, -(-part // chunk))
     return segs, part, nloops
+
+
+def ring_members(meta: CollMeta, nranks: int) -> tuple:
+    """Parent ranks of the collective's ring, in ring order."""
+    return tuple(meta.members) if meta.members is not None else tuple(range(nranks))
 
 
 def slice_range(st: _Static, q: int, loop: int, slc: int, cfg: SimConfig):
@@ -394,10 +402,12 @@ class Simulator:
     def _admit(self, r: int, b: int, sqe: _Sqe):
         R, L = self.ranks[r], self.ranks[r].lanes[b]
         m = sqe.meta
-        segs, part, nloops = lane_geometry(m, self.n, r, self.cfg)
-        seq = ring.ring_sequence(m.kind, self.n, r, m.root, m.inplace)
-        R.static[(m.coll_id, b)] = _Static(m, r, self.n, seq, segs, part, b, nloops,
-                                           sqe.sendbuf, sqe.recvbuf, sqe.sub_index)
+        members = ring_members(m, self.n)
+        n, rr = len(members), members.index(r)          # the collective's own ring size / rank
+        segs, part, nloops = lane_geometry(m, n, rr, self.cfg)
+        seq = ring.ring_sequence(m.kind, n, rr, m.root, m.inplace)
+        R.static[(m.coll_id, b)] = _Static(m, rr, n, seq, segs, part, b, nloops,
+                                           sqe.sendbuf, sqe.recvbuf, sqe.sub_index, members)
         R.dyn_global[(m.coll_id, b)] = _Dyn()
         way = m.coll_id % self.cfg.cache_ways
         if way in L.cache and L.cache[way][0] == m.coll_id:
@@ -431,8 +441,9 @@ class Simulator:
         prim, q = st.seq[d.step]
         recv, reduce_, copy, send = ring.PRIMS[prim]
         m = st.meta
-        n = self.n
-        cin = self._connector(m.coll_id, b, (r - 1) % n) if recv else None
+        n, mem = st.n, st.members
+        # connector (coll, lane, writer): written by the ring predecessor, a parent rank
+        cin = self._connector(m.coll_id, b, mem[(st.rank - 1) % n]) if recv else None
         cout = self._connector(m.coll_id, b, r) if send else None
         if recv and not cin.can_pop():
             return False
@@ -613,17 +624,20 @@ class Simulator:
 def plan_transfers(meta: CollMeta, n: int, cfg: SimConfig):
     """Planned slice transfers per (lane, step) for one submission: nloops * slices."""
     out = {}
-    for r in range(n):
+    members = ring_members(meta, n)
+    for r in members:
+        rr, ns = members.index(r), len(members)
         for b in range(meta.nblocks):
-            _, _, nloops = lane_geometry(meta, n, r, cfg)
-            seq = ring.ring_sequence(meta.kind, n, r, meta.root, meta.inplace)
+            _, _, nloops = lane_geometry(meta, ns, rr, cfg)
+            seq = ring.ring_sequence(meta.kind, ns, rr, meta.root, meta.inplace)
             for j in range(len(seq)):
                 out[(r, b, j)] = nloops * cfg.slices_per_chunk
     return out
 
 
 def make_buffers(meta: CollMeta, n: int, seed: int):
-    """Per-rank (sendbuf, recvbuf) from the shared generator (nccl-tests conventions)."""
+    """Per-rank (sendbuf, recvbuf) from the shared generator (nccl-tests conventions);
+    for a sub-communicator, n is its ring size and index r its ring rank."""
     from inputs import hashgen
     xs = ring.inputs_full(meta.kind, meta.dtype, n, meta.count, seed, meta.coll_id)
     outs = []
@@ -653,9 +667,10 @@ def run_orders(metas, orders, cfg: SimConfig, seed: int = 1, iterations: int = 1
     programs = [[] for _ in range(n)]
     for it in range(iterations):
         for m in metas:
-            xs, outs = make_buffers(m, n, seed + it)
-            for r in range(n):
-                bufs[(r, m.coll_id, it)] = (xs[r], outs[r])
+            mem = ring_members(m, n)
+            xs, outs = make_buffers(m, len(mem), seed + it)
+            for k, r in enumerate(mem):
+                bufs[(r, m.coll_id, it)] = (xs[k], outs[k])
         for r in range(n):
             for k, cid in enumerate(orders[r]):
                 m = metas[cid]

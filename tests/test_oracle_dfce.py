@@ -334,3 +334,68 @@ def test_context_cache_and_lazy_save_accounting():
     sim, _ = dfce.run_orders(metas, orders, cfg, seed=1)
     assert sim.saves <= sim.total_preemptions()
     assert sim.loads >= 1
+
+
+# ------------------------------------------------------------------ sub-communicators
+def _sub_metas():
+    """Overlapping rings on 3 ranks: A = {0,1}, B = {1,2}, C = {2,0} (a cycle of
+    pairwise groups) and D = all ranks -- every pair of groups overlaps."""
+    return [dfce.CollMeta(0, "allreduce", "f32", 40, members=(0, 1)),
+            dfce.CollMeta(1, "allreduce", "i32", 33, members=(1, 2)),
+            dfce.CollMeta(2, "allgather", "f32", 9, members=(2, 0)),
+            dfce.CollMeta(3, "reducescatter", "bf16", 12)]
+
+
+def _sub_order_sets(metas, n):
+    per_rank = [[m.coll_id for m in metas if r in dfce.ring_members(m, n)] for r in range(n)]
+    return [list(map(list, combo)) for combo in itertools.product(*[itertools.permutations(p) for p in per_rank])]
+
+
+def _check_sub_results(sim, bufs, metas, n):
+    for m in metas:
+        mem = dfce.ring_members(m, n)
+        xs = [bufs[(r, m.coll_id, 0)][0] for r in mem]
+        exp = ring.result_full(m.kind, m.dtype, xs, root=m.root)   # the sub-ring's own O1 result
+        for k, r in enumerate(mem):
+            got = sim.results[(r, m.coll_id, 0)]
+            assert np.array_equal(_bits(got), _bits(exp[k])), (m.coll_id, r)
+
+
+def test_subcommunicators_all_orders_complete():
+    """Overlapping sub-communicator rings on one daemon per rank: every per-rank
+    order set (each rank orders only its own collectives) completes with the
+    sub-ring's exact result, exactly once (liveness I1 holds per ring; admission I4
+    is per rank)."""
+    n, metas = 3, _sub_metas()
+    sets = _sub_order_sets(metas, n)
+    assert len(sets) == 6 ** 3
+    for si, orders in enumerate(sets):
+        T = (1, 3, 64)[si % 3]
+        cfg = dfce.SimConfig(spin_base=T, spin_step=max(1, T // 8), spin_min=1, spin_cap=4 * T,
+                             stickiness=bool(si % 2), order_policy=("fifo", "priority")[(si // 2) % 2],
+                             seed=si, **_BF_CFG)
+        sim, bufs = dfce.run_orders(metas, orders, cfg, seed=si)
+        _check_sub_results(sim, bufs, metas, n)
+        for r in range(n):
+            assert len(sim.ranks[r].cq) == sim.ranks[r].submitted
+        for m in metas:
+            plan = dfce.plan_transfers(m, n, sim.cfg)
+            for (r, b, j), cnt in plan.items():
+                assert sim.transfers[(r, m.coll_id, 0, b, j)] == cnt
+
+
+def test_subcommunicators_baseline_deadlocks_on_cyclic_orders():
+    """Negative control: the NCCL-like baseline deadlocks when the pairwise groups
+    are started in a cyclic order (0 waits for 1 on A, 1 for 2 on B, 2 for 0 on C)
+    -- the hybrid-parallel hazard sub-communicators bring -- and completes when all
+    ranks follow one global order."""
+    n = 3
+    metas = _sub_metas()[:3]
+    cyclic = [[0, 2], [1, 0], [2, 1]]       # rank 0: A then C; rank 1: B then A; rank 2: C then B
+    with pytest.raises(dfce.Deadlock):
+        dfce.run_orders(metas, cyclic, dfce.SimConfig(baseline=True, seed=1, **_BF_CFG), seed=2)
+    consistent = [[0, 2], [0, 1], [1, 2]]   # ids ascending on every rank
+    sim, bufs = dfce.run_orders(metas, consistent, dfce.SimConfig(baseline=True, seed=1, **_BF_CFG), seed=2)
+    _check_sub_results(sim, bufs, metas, n)
+    sim, bufs = dfce.run_orders(metas, cyclic, dfce.SimConfig(seed=1, **_BF_CFG), seed=2)   # OCCL: fine
+    _check_sub_results(sim, bufs, metas, n)
