@@ -495,7 +495,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->spinMin = 128;
   c->spinBoost = 2;
   c->spinCap = 65536;
-  c->spinNs = 40;                         // measured cost of a failed head poll (R1)
+  c->spinNs = 150;                        // one spin ~ an L2 round trip of a flag poll under load (R1)
   c->stallLimit = 2;
   c->quitEnabled = 1;
   c->quitIdleNs = 1'000'000;

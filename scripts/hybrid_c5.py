@@ -69,14 +69,25 @@ def main():
     ap.add_argument("--mib", type=float, default=16.0)
     ap.add_argument("--seeds", type=int, default=3)
     ap.add_argument("--out", default="gpurun_out/c5_hybrid")
+    ap.add_argument("--slice-kib", type=int, default=0, help="0 = library default")
+    ap.add_argument("--ll-max", type=int, default=-1, help="-1 = library default")
+    ap.add_argument("--policies", default="1,0")
+    ap.add_argument("--spin-ns", type=int, default=0, help="0 = library default")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     n = 8
     jobs, tp, pp = build(args.nmb)
     count = int(args.mib * (1 << 20)) // 2
     rows = []
-    for policy in (1, 0):
-        comms = harness.ring(n, 0, gridBlocks=16, maxColl=256, autoLaunch=0, orderPolicy=policy)
+    extra = {}
+    if args.slice_kib:
+        extra["sliceBytes"] = args.slice_kib << 10
+    if args.ll_max >= 0:
+        extra["llMaxBytes"] = args.ll_max
+    if args.spin_ns:
+        extra["spinNs"] = args.spin_ns
+    for policy in [int(x) for x in args.policies.split(",")]:
+        comms = harness.ring(n, 0, gridBlocks=16, maxColl=256, autoLaunch=0, orderPolicy=policy, **extra)
         subs = {}
         for gi, g in enumerate(tp):
             subs[("tp", gi)] = [comms[q].split(g) for q in g]

@@ -52,6 +52,7 @@ def main():
     ap.add_argument("--seeds", type=int, default=3)
     ap.add_argument("--workloads", default="c3,resnet50-buckets,resnet50-tensors,bert-large-buckets")
     ap.add_argument("--out", default="gpurun_out/c3_c4")
+    ap.add_argument("--spin-ns", type=int, default=0, help="0 = library default")
     ap.add_argument("--variants", default="priority:1,fifo:1,fifo:0",
                     help="order_policy:stickiness pairs")
     args = ap.parse_args()
@@ -63,7 +64,7 @@ def main():
             pol, stick = var.split(":")
             policy, stick = (1 if pol == "priority" else 0), int(stick)
             comms = harness.ring(n, 0, gridBlocks=18, maxColl=256, autoLaunch=0, stickiness=stick,
-                                 orderPolicy=policy)
+                                 orderPolicy=policy, **({"spinNs": args.spin_ns} if args.spin_ns else {}))
             for seed in range(args.seeds):
                 colls, orders = workload(wname, n, seed)
                 bufs = {c.coll_id: harness.buffers(c.kind, c.dtype, n, c.count, comms) for c in colls}
