@@ -360,6 +360,7 @@ struct Sched {
   uint64_t cursor, lastFetch, iter;
   uint64_t T, headSeen, creditSeen;
   uint32_t qlen, pos, exiting;
+  uint32_t rr;                 // priority policy: next non-front entry to visit
   int lastRun, curId;
   int way;
   unsigned long long cycRun, cycPoll, cycAcqFence, cycRelFence, nCommit;   // probes
@@ -593,7 +594,20 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
       uint32_t st = m.tq[sh.pos] >> 16;
       if (st < 0xffff) ++st;
       m.tq[sh.pos] = (m.tq[sh.pos] & 0xffffu) | (st << 16);
-      sh.pos = (sh.pos + 1) % sh.qlen;
+      if (p.orderPolicy == 1 && sh.qlen > 1) {
+        // priority order (reading R10): the traversal interleaves the queue front
+        // with the other entries (0, r1, 0, r2, ...) -- fair, but the highest-
+        // priority collective is retried every other switch, so ranks re-converge
+        // on the same front quickly after a straggler shows up
+        if (sh.pos != 0) {
+          sh.pos = 0;
+        } else {
+          if (sh.rr == 0 || sh.rr >= sh.qlen) sh.rr = 1;
+          sh.pos = sh.rr++;
+        }
+      } else {
+        sh.pos = (sh.pos + 1) % sh.qlen;
+      }
     }
     sh.lastRun = -1;
   }
@@ -1286,6 +1300,7 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
     sh.pos = bs.pos;
     sh.exiting = bs.exiting;
     sh.iter = 0;
+    sh.rr = 1;
     sh.lastRun = -1;
     sh.curId = -1;
     sh.cycRun = sh.cycPoll = sh.cycAcqFence = sh.cycRelFence = sh.nCommit = 0;
