@@ -295,7 +295,9 @@ def run_occl(args):
                                            ("cycRun", "cycPoll", "cycAcqFence", "cycRelFence")},
                      "per_slice_data_cycles": round(probes["cycData"] / nd, 1),
                      "per_slice_datawait_cycles": round(probes["cycDataWait"] / nd, 1),
-                     "commits": probes["nCommit"], "data_slices_timed": probes["nData"]}
+                     "commits": probes["nCommit"], "data_slices_timed": probes["nData"],
+                     "publisher_fences": probes["nFence"],
+                     "cycles_per_release_fence": round(probes["cycRelFence"] / max(1, probes["nFence"]), 1)}
     if dist is not None:
         t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -133,11 +133,16 @@ typedef struct {
   uint64_t cycRun;        /* control thread inside collective runs                  */
   uint64_t cycPoll;       /* ... in failed connector polls (waiting for peers)      */
   uint64_t cycAcqFence;   /* ... in the acquire fence after a successful poll       */
-  uint64_t cycRelFence;   /* ... in the commit (release) fence                      */
+  uint64_t cycRelFence;   /* publisher lanes in release fences                      */
   uint64_t cycData;       /* data-group leader threads moving slices                */
   uint64_t cycDataWait;   /* data-group leader threads waiting for a descriptor     */
   uint64_t nData;         /* slices timed by data-group leaders                     */
   uint64_t nCommit;       /* slices committed                                       */
+  uint64_t nFence;        /* release fences issued by publisher lanes               */
+  uint64_t cycCtxLoad;    /* context loads into the shared-memory cache */
+  uint64_t nCtxLoad;
+  uint64_t cycCtxSave;    /* lazy dynamic-context saves              */
+  uint64_t nCtxSave;
 } occlProbes_t;
 
 /* One device trace record (%globaltimer ns).  tag = event << 24 | collId; for

@@ -358,12 +358,13 @@ constexpr int kTmaMinBytes = 16384;    // slices below this use register loads (
 // Scheduler state of one block; touched only by the control thread.
 struct Sched {
   uint64_t cursor, lastFetch, iter;
-  uint64_t T, headSeen, creditSeen;
+  uint64_t T;
   uint32_t qlen, pos, exiting;
   uint32_t rr;                 // priority policy: next non-front entry to visit
   int lastRun, curId;
   int way;
   unsigned long long cycRun, cycPoll, cycAcqFence, cycRelFence, nCommit;   // probes
+  unsigned long long cycCtxLoad, nCtxLoad, cycCtxSave, nCtxSave;
 };
 
 // Control -> data warp pipeline: slice descriptors in a ring of `depth` buffers.
@@ -586,7 +587,10 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
       // preempted: lazy save of a dynamic context that progressed
       if (cx.d.progressed) {
         cx.d.progressed = 0;
-        save_dyn(g, cx.d);
+        const long long t0 = clock64();
+        save_dyn(g, cx.d);                           // probe: the paper's 0.05 us save
+        sh.cycCtxSave += clock64() - t0;
+        ++sh.nCtxSave;
         cs.ctxSaves++;
       }
       cs.preemptions++;
@@ -673,6 +677,7 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
       // context load into the shared-memory cache: 8 independent 16-B loads in
       // flight
       m.cacheTag[way] = c;
+      const long long t0 = clock64();
       const uint4* gsrc = reinterpret_cast<const uint4*>(&p.ctx[(size_t)c * G + b]);
       uint4 v[kCtxBytes / 16];
 #pragma unroll
@@ -680,6 +685,8 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
       uint4* dst = reinterpret_cast<uint4*>(&m.cache[way]);
 #pragma unroll
       for (int i = 0; i < kCtxBytes / 16; ++i) dst[i] = v[i];
+      sh.cycCtxLoad += clock64() - t0;                 // probe: the paper's 0.45 us load
+      ++sh.nCtxLoad;
       p.collStats[(size_t)c * G + b].ctxLoads++;
     }
     sh.curId = c;
@@ -775,7 +782,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   // an LL poll (a 16-B line in L2) and a cached head poll differ 10x in cost
   uint64_t T = sh.T, spinStart = 0;
   const uint64_t spinNs = p.spinNs;
-  unsigned long long nSlices = 0, cPoll = 0, cFence = 0;
+  unsigned long long nSlices = 0, cPoll = 0;
   const long long tRun = clock64();
   trace_at(p, *m.tr, b, kEvSwitchIn, sh.curId, sh.pos);
   int run;
@@ -921,7 +928,6 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   sh.T = T;
   sh.cycRun += clock64() - tRun;
   sh.cycPoll += cPoll;
-  sh.cycRelFence += cFence;
   sh.nCommit += nSlices;
   p.collStats[cb].slices += nSlices;
   return run;
@@ -943,8 +949,11 @@ __device__ __noinline__ void control_main(const DaemonParams& p, int b, Sched& s
   bst.cycRun += sh.cycRun;
   bst.cycPoll += sh.cycPoll;
   bst.cycAcqFence += sh.cycAcqFence;
-  bst.cycRelFence += sh.cycRelFence;
   bst.nCommit += sh.nCommit;
+  bst.cycCtxLoad += sh.cycCtxLoad;
+  bst.nCtxLoad += sh.nCtxLoad;
+  bst.cycCtxSave += sh.cycCtxSave;
+  bst.nCtxSave += sh.nCtxSave;
   // release the data warps (the pipe is drained after every run)
   pipe.ring[issued % D].prim = P_EXIT;
   mbar_arrive(&pipe.full[issued % D]);
@@ -1215,6 +1224,7 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
 // (commit visibility).
 __device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& pipe) {
   const uint32_t D = (uint32_t)p.pipeDepth;
+  unsigned long long cycFence = 0, nFence = 0;
   const int sys = p.sysScope;
   uint32_t j = 0;
   for (;;) {
@@ -1222,6 +1232,8 @@ __device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& 
     mbar_wait(&pipe.full[i], (j / D) & 1);
     if (pipe.ring[i].prim == P_EXIT) {
       if (p.traceCap) p.traceCount[b] = pipe.tr.base + pipe.tr.idx;   // control traced its last record already
+      atomicAdd(&p.blkStats[b].cycRelFence, cycFence);                // release-fence probe (publisher lane)
+      atomicAdd(&p.blkStats[b].nFence, nFence);
       break;
     }
     mbar_wait(&pipe.sdone[i], (j / D) & 1);
@@ -1247,7 +1259,12 @@ __device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& 
       k = k1;
     }
     trace_at(p, pipe.tr, b, kEvSdone, k - j + 1, (uint32_t)(hv & 0xffff) | ((uint32_t)(cv & 0xffff) << 16));
-    if (needFence) fence_acq_rel(sys);
+    if (needFence) {                            // LL data carries its own flags: no release needed
+      const long long tf = clock64();
+      fence_acq_rel(sys);
+      cycFence += clock64() - tf;
+      ++nFence;
+    }
     if (send) red_max_relaxed(ho, hv, sys);     // head of rank r+1
     if (recv) red_max_relaxed(co, cv, sys);     // credit of rank r-1
     trace_at(p, pipe.tr, b, kEvPublish, k - j + 1, (uint32_t)(hv & 0xffff) | ((uint32_t)(cv & 0xffff) << 16));
@@ -1304,6 +1321,7 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
     sh.lastRun = -1;
     sh.curId = -1;
     sh.cycRun = sh.cycPoll = sh.cycAcqFence = sh.cycRelFence = sh.nCommit = 0;
+    sh.cycCtxLoad = sh.nCtxLoad = sh.cycCtxSave = sh.nCtxSave = 0;
     for (uint32_t i = 0; i < sh.qlen; ++i) {
       m.tq[i] = p.tqSave[(size_t)b * p.maxColl + i];
       const int c = (int)(m.tq[i] & 0xffffu);

@@ -1041,6 +1041,11 @@ occlResult_t occlGetProbes(occlComm_t c, occlProbes_t* out) {
     out->cycPoll += b.cycPoll;
     out->cycAcqFence += b.cycAcqFence;
     out->cycRelFence += b.cycRelFence;
+    out->nFence += b.nFence;
+    out->cycCtxLoad += b.cycCtxLoad;
+    out->nCtxLoad += b.nCtxLoad;
+    out->cycCtxSave += b.cycCtxSave;
+    out->nCtxSave += b.nCtxSave;
     out->cycData += b.cycData;
     out->cycDataWait += b.cycDataWait;
     out->nData += b.nData;

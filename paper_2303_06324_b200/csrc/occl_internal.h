@@ -101,17 +101,20 @@ struct alignas(16) CollStat {   // per (collective, block), device memory
   unsigned long long preemptions, ctxLoads, ctxSaves, slices, completions, pad[3];
 };
 struct alignas(16) BlockStat {  // per block
-  unsigned long long quits, exits, fetched, cqes, launches, idlePolls, pad[2];
+  unsigned long long quits, exits, fetched, cqes, launches, idlePolls, pad[1];
   // in-kernel timing probes (SM clock cycles), flushed when the block exits
   // (the paper's "core execution time" probes)
   unsigned long long cycRun;        // control thread inside collective runs
   unsigned long long cycPoll;       // ... in failed connector polls (waiting for peers)
   unsigned long long cycAcqFence;   // ... in the acquire fence after a successful poll
-  unsigned long long cycRelFence;   // ... in the commit (release) fence
+  unsigned long long cycRelFence;   // publisher lane in release fences
+  unsigned long long nFence;        // release fences issued by the publisher lane
   unsigned long long cycData;       // data group leaders: moving slices
   unsigned long long cycDataWait;   // data group leaders: waiting for a descriptor
   unsigned long long nData;         // slices timed by data group leaders
   unsigned long long nCommit;       // slices committed
+  unsigned long long cycCtxLoad, nCtxLoad;   // context loads (cache misses) by the control lane
+  unsigned long long cycCtxSave, nCtxSave;   // lazy dynamic-context saves
 };
 
 // Device event trace (one ring of `traceCap` records per block, %globaltimer

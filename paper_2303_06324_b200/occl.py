@@ -70,7 +70,8 @@ class occlTraceRec_t(C.Structure):
 
 class occlProbes_t(C.Structure):
     _fields_ = [(k, C.c_uint64) for k in ("cycRun", "cycPoll", "cycAcqFence", "cycRelFence", "cycData",
-                                          "cycDataWait", "nData", "nCommit")]
+                                          "cycDataWait", "nData", "nCommit", "nFence", "cycCtxLoad",
+                                          "nCtxLoad", "cycCtxSave", "nCtxSave")]
 
 
 CALLBACK = C.CFUNCTYPE(None, C.c_int, C.c_void_p)

@@ -45,6 +45,7 @@ def main():
         for c in comms:
             c.trace_reset()
         before = [c.stats() for c in comms]
+        pb = [c.probes() for c in comms]
         stream = torch.cuda.ExternalStream(comms[0].stream(), device=0)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         for r in range(1, n):                            # everybody but the straggler
@@ -70,6 +71,10 @@ def main():
         ms = e0.elapsed_time(e1)
         after = [c.stats() for c in comms]
         d = {k: sum(a[k] - b[k] for a, b in zip(after, before)) for k in ("preemptions", "ctxLoads", "ctxSaves")}
+        pa = [c.probes() for c in comms]
+        pr = {k: sum(a[k] - b0[k] for a, b0 in zip(pa, pb)) for k in pa[0]}
+        d["ctx_load_us"] = pr["cycCtxLoad"] / max(1, pr["nCtxLoad"]) / 1965.0   # SM clock ~1965 MHz
+        d["ctx_save_us"] = pr["cycCtxSave"] / max(1, pr["nCtxSave"]) / 1965.0
         tr = comms[1].trace(0)
         sw = [a for t, ev, c, a in tr if ev == "switch_in"]
         pre = sum(1 for t, ev, c, a in tr if ev == "preempt")
