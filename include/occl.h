@@ -75,7 +75,7 @@ typedef enum { occlOrderFifo = 0, occlOrderPriority = 1 } occlOrderPolicy_t;
 typedef struct {
   int maxColl;            /* registry size: collId in [0, maxColl) ("up to 1,000")   */
   int gridBlocks;         /* G: daemon grid = max blocks any collective uses        */
-  int blockThreads;       /* threads per block: control, TMA and publisher warps + compute warps (128..640) */
+  int blockThreads;       /* threads per block: control, TMA and publisher warps + compute warps (128..608) */
   int connSlots;          /* K: slots per connector; must exceed slicesPerChunk                    */
   int slicesPerChunk;     /* slices each primitive moves per loop             */
   size_t sliceBytes;      /* bytes per connector slot (multiple of 16)                             */
@@ -101,7 +101,7 @@ typedef struct {
   int l2Hints;            /* 1 = evict-first L2 policy for send/recv-buffer streams               */
   int directMode;         /* 1 = final data goes straight into a same-process peer's recv buffer  */
   int stagingTiles;       /* TMA staging ring depth per block (1..6), 32 KiB of shared memory each */
-  int blocksPerSM;        /* 1 (up to 640 threads) or 2 (up to 384 threads, <= 3 staging tiles)    */
+  int blocksPerSM;        /* 1 (up to 608 threads) or 2 (up to 384 threads, <= 3 staging tiles)    */
   uint32_t traceCap;      /* device event-trace records kept per block (0 = tracing off)          */
   uint32_t llSliceBytes;  /* LL protocol: payload bytes per slice (multiple of 8; lines are 16 B) */
   uint32_t llMaxBytes;    /* a collective whose per-block part is <= this uses LL (0 = never)   */
