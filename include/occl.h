@@ -106,6 +106,7 @@ typedef struct {
   uint32_t llSliceBytes;  /* LL protocol: payload bytes per slice (multiple of 8; lines are 16 B) */
   uint32_t llMaxBytes;    /* a collective whose per-block part is <= this uses LL (0 = never)   */
   uint32_t spinNs;        /* one spin = this many ns of failed polling (thresholds are in spins)  */
+  int bulkStores;         /* 1 = staged tiles are stored with cp.async.bulk by the publisher lane  */
 } occlConfig_t;
 
 /* Aggregate counters (device counters summed over blocks/collectives). */

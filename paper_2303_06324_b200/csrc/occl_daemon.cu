@@ -985,6 +985,20 @@ __device__ __forceinline__ void st_cg_hint(void* p, const uint4& v, uint64_t pol
   asm volatile("st.global.cg.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;"
                :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
 }
+// Bulk (TMA) store shared -> global, tracked by the issuing thread's bulk groups.
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               :: "l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_store_hint(void* gdst, const void* ssrc, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+               :: "l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // Invalidate a consumed connector line in L2 without writing it back: the slot
 // is rewritten by the upstream before anyone reads it again (PTX `discard`
 // behaves like a weak write, so the credit's release orders it before the
@@ -1125,9 +1139,20 @@ __device__ __forceinline__ void ll_slice(const int prim, const char* src, const 
 // Compute warps: every compute warp takes part in every slice, in order.  The
 // descriptor is read field by field into registers (a struct copy would live in
 // local memory and be re-read in the inner loop).
+template <int DT>
+__device__ __forceinline__ void reduce_tile_smem(Stage& st, int sz, int tid, int nt) {
+  const int nv = sz >> 4;
+  for (int i = tid; i < nv; i += nt) {
+    const uint4 v = vadd<DT>(lds_v4(&st.in[i]), lds_v4(&st.loc[i]));
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" :: "r"(smem_u32(&st.in[i])), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w) : "memory");
+  }
+}
+
 __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pipe, Stage* stages, uint64_t* tfull,
-                                          uint64_t* tempty, const int ctid, const int cnt) {
+                                          uint64_t* tempty, uint64_t* tred, const int ctid, const int cnt) {
   const uint32_t D = (uint32_t)p.pipeDepth, S = (uint32_t)p.stages;
+  const bool bulk = p.bulkStores != 0;
   const int lane = ctid & 31;
   const bool hints = p.l2Hints != 0, discard = p.discardConsumed != 0;
   const uint64_t pol = policy_evict_first();
@@ -1168,6 +1193,21 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
         if (++cs == S) { cs = 0; cph ^= 1; }
         const int sz = min(kTile, vb - off);
         if (disc && ctid < (sz >> 7)) discard_l2_line(cin + off + ((size_t)ctid << 7));  // tile is in smem now
+        if (bulk) {
+          // bulk-store mode: reduce in place in shared memory; the publisher lane
+          // stores the tile with cp.async.bulk (copy tiles need no compute at all)
+          if (prim & A_REDUCE) {
+            if (dtype == kF32) reduce_tile_smem<kF32>(stages[s], sz, ctid, cnt);
+            else if (dtype == kBF16) reduce_tile_smem<kBF16>(stages[s], sz, ctid, cnt);
+            else reduce_tile_smem<kI32>(stages[s], sz, ctid, cnt);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> async proxy
+          }
+          // every tile (copy tiles too) completes one tred phase, so tred[s] stays
+          // in step with the stage's phase
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tred[s]);
+          continue;
+        }
         if (prim & A_REDUCE) {
           if (dtype == kF32) consume_tile<kF32>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol);
           else if (dtype == kBF16) consume_tile<kBF16>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol);
@@ -1222,10 +1262,14 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
 // covered by the same release fence; then the head of the downstream rank and
 // the credit of the upstream rank are raised to the last slice's values
 // (commit visibility).
-__device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& pipe) {
-  const uint32_t D = (uint32_t)p.pipeDepth;
+__device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& pipe, Stage* stages, uint64_t* tfull,
+                                            uint64_t* tempty, uint64_t* tred) {
+  const uint32_t D = (uint32_t)p.pipeDepth, S = (uint32_t)p.stages;
   unsigned long long cycFence = 0, nFence = 0;
   const int sys = p.sysScope;
+  const bool bulk = p.bulkStores != 0, hints = p.l2Hints != 0;
+  const uint64_t pol = policy_evict_first();
+  uint32_t cs = 0, cph = 0;                         // bulk mode: staging slot / phase (same walk as the producer)
   uint32_t j = 0;
   for (;;) {
     const uint32_t i = j % D;
@@ -1236,7 +1280,42 @@ __device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& 
       atomicAdd(&p.blkStats[b].nFence, nFence);
       break;
     }
+    bool bulkSlice = false;
+    if (bulk) {
+      // bulk-store mode: this lane stores every staged tile of a TMA-path slice
+      // (cp.async.bulk, one group per tile), hands each stage back once its
+      // store has read it, and publishes after the slice's writes completed --
+      // the release fence then waits for no generic stores at all
+      const SliceDesc& d = pipe.ring[i];
+      const int vb = (d.prim & (A_COPY | A_SEND)) && !(d.prim & A_LL)
+                         ? tma_vec_bytes(d.dtype, d.nelem, d.src, d.dst, d.cout) : 0;
+      if (vb > 0) {
+        bulkSlice = true;
+        const bool copy = d.prim & A_COPY, send = d.prim & A_SEND;
+        int prev = -1;
+        for (int off = 0; off < vb; off += kTile) {
+          const uint32_t st = cs, ph = cph;
+          if (++cs == S) { cs = 0; cph ^= 1; }
+          const uint32_t sz = (uint32_t)min(kTile, vb - off);
+          mbar_wait(&tred[st], ph);                   // tile staged (and reduced in place)
+          if (copy) {
+            if (hints) bulk_store_hint(d.dst + off, stages[st].in, sz, pol);
+            else bulk_store(d.dst + off, stages[st].in, sz);
+          }
+          if (send) bulk_store(d.cout + off, stages[st].in, sz);
+          bulk_commit();
+          if (prev >= 0) {
+            bulk_wait_read1();                       // the previous tile's stores have read their stage
+            mbar_arrive(&tempty[prev]);
+          }
+          prev = (int)st;
+        }
+        bulk_wait_read0();
+        mbar_arrive(&tempty[prev]);
+      }
+    }
     mbar_wait(&pipe.sdone[i], (j / D) & 1);
+    if (bulkSlice) bulk_wait_all();                  // the slice's bulk writes are complete
     bool send = false, recv = false, needFence = false;
     uint64_t hv = 0, cv = 0;
     char* ho = nullptr;
@@ -1250,6 +1329,7 @@ __device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& 
       // follow loads that already returned their values
       if ((d.prim & (A_SEND | A_RECV)) && !(d.prim & A_LL)) needFence = true;
       const uint32_t k1 = k + 1;
+      if (bulk) break;                              // bulk mode publishes slice by slice
       if (!mbar_test(&pipe.full[k1 % D], (k1 / D) & 1)) break;
       const SliceDesc& d1 = pipe.ring[k1 % D];
       if (d1.prim == P_EXIT) break;
@@ -1296,7 +1376,7 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Sched sh;
   __shared__ Pipe pipe;
-  __shared__ uint64_t tfull[kMaxStages], tempty[kMaxStages];
+  __shared__ uint64_t tfull[kMaxStages], tempty[kMaxStages], tred[kMaxStages];
   const int W = p.cacheWays;
   Stage* stages = reinterpret_cast<Stage*>(smem);                       // 128-B aligned
   Smem m;
@@ -1338,7 +1418,8 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
     }
     for (int i = 0; i < p.stages; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], nComputeWarps);
+      mbar_init(&tempty[i], p.bulkStores ? 1 : nComputeWarps);   // bulk mode: the storing lane frees stages
+      mbar_init(&tred[i], nComputeWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     p.blkStats[b].launches++;
@@ -1348,10 +1429,10 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
   if (tid < 32 * kRoleWarps) {
     if (tid == 0) control_main(p, b, sh, m, pipe);
     else if (tid == 32) producer_main(p, pipe, stages, tfull, tempty);
-    else if (tid == 64) publisher_main(p, b, pipe);
+    else if (tid == 64) publisher_main(p, b, pipe, stages, tfull, tempty, tred);
     return;
   }
-  compute_main(p, b, pipe, stages, tfull, tempty, tid - 32 * kRoleWarps, nComputeWarps * 32);
+  compute_main(p, b, pipe, stages, tfull, tempty, tred, tid - 32 * kRoleWarps, nComputeWarps * 32);
 }
 
 extern "C" size_t occl_internal_daemon_smem(int maxColl, int cacheWays, int stages) {

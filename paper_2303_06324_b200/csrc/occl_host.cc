@@ -495,6 +495,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->spinMin = 128;
   c->spinBoost = 2;
   c->spinCap = 65536;
+  c->bulkStores = 0;
   c->spinNs = 150;                        // one spin ~ an L2 round trip of a flag poll under load (R1)
   c->stallLimit = 2;
   c->quitEnabled = 1;
@@ -733,6 +734,7 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   p.traceCount = c->traceCount;
   p.traceCap = c->cfg.traceCap;
   p.stages = c->cfg.stagingTiles;
+  p.bulkStores = c->cfg.bulkStores;
   p.blocksPerSM = c->cfg.blocksPerSM;
   p.l2Hints = c->cfg.l2Hints;
   Launcher* L = new Launcher();

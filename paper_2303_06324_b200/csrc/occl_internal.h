@@ -173,6 +173,7 @@ struct DaemonParams {
   uint32_t llSliceBytes;            // LL payload per slice (lines carry 8 B payload + 8 B flags)
   uint32_t llMaxBytes;              // a collective uses LL when its per-block part is at most this
   int stages;                       // TMA staging tiles per block (x 2 x 16 KiB of shared memory)
+  int bulkStores;                   // 1: staged tiles leave through cp.async.bulk stores (publisher lane)
   int blocksPerSM;                  // 1 or 2 co-resident daemon blocks per SM
   int l2Hints;                      // evict-first L2 policy for user-buffer loads / stores
 };
