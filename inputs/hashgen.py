@@ -16,6 +16,9 @@ so no rounding happens during generation and the GPU generator in
 * ``bf16``: m = u >> 56 (8 bits),  e = (u >> 32) & 7,
             x = (m - 128) * 2^(-7 - e)            exact in bf16 (<= 8 sig. bits);
             returned as uint16 bit patterns (numpy has no bfloat16).
+* ``f16`` : m = u >> 53 (11 bits), e = (u >> 32) & 7,
+            x = (m - 1024) * 2^(-10 - e)          exact in IEEE binary16 (11 sig. bits,
+            2^-17 >= the smallest normal's ulp range); stored as numpy float16.
 * ``i32`` : low 32 bits of u, as two's-complement int32.
 
 This module holds no arithmetic of the collective method.
@@ -26,9 +29,9 @@ import numpy as np
 
 MASK64 = (1 << 64) - 1
 
-DTYPES = ("i32", "f32", "bf16")
-ITEMSIZE = {"i32": 4, "f32": 4, "bf16": 2}
-NP_STORAGE = {"i32": np.int32, "f32": np.float32, "bf16": np.uint16}
+DTYPES = ("i32", "f32", "bf16", "f16")
+ITEMSIZE = {"i32": 4, "f32": 4, "bf16": 2, "f16": 2}
+NP_STORAGE = {"i32": np.int32, "f32": np.float32, "bf16": np.uint16, "f16": np.float16}
 
 
 def splitmix64(x: np.ndarray) -> np.ndarray:
@@ -59,6 +62,9 @@ def values(dtype: str, seed: int, coll: int, rank: int, idx) -> np.ndarray:
         m = (u >> np.uint64(56)).astype(np.int64) - 128
         f = np.ldexp(m.astype(np.float64), -7 - e).astype(np.float32)
         return (f.view(np.uint32) >> np.uint32(16)).astype(np.uint16)
+    if dtype == "f16":
+        m = (u >> np.uint64(53)).astype(np.int64) - 1024
+        return np.ldexp(m.astype(np.float64), -10 - e).astype(np.float16)
     raise ValueError(f"unknown dtype {dtype!r}")
 
 

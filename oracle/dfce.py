@@ -93,6 +93,7 @@ class CollMeta:
     inplace: bool = False
     priority: int | None = None    # priority policy: globally agreed, lower first (default coll_id)
     members: tuple | None = None   # sub-communicator ring (parent ranks in ring order); None = all
+    op: str = "sum"                # reducing function
                                    # (the static context carries nranks / rank)
 
 
@@ -196,14 +197,14 @@ class Deadlock(Exception):
 
 
 # ============================================================================ pure pieces
-def apply_action_set(prim: str, incoming, local, dtype: str):
+def apply_action_set(prim: str, incoming, local, dtype: str, op: str = "sum"):
     """Fused actions of one primitive on one slice:
     recv grabs ``incoming`` from the recv connector, reduce combines it with the
     send-buffer slice ``local``, copy puts the value into the recv buffer, send pushes
     it to the send connector.  Returns (to_recv_buf | None, to_send_conn | None)."""
     recv, reduce_, copy, send = ring.PRIMS[prim]
     if recv and reduce_:
-        val = ring.add(incoming, local, dtype)
+        val = ring.add(incoming, local, dtype, op)
     elif recv:
         val = incoming
     else:
@@ -457,7 +458,7 @@ class Simulator:
         local = None
         if (reduce_ or not recv) and prim != "Recv":
             local = st.sendbuf[send_base + lo: send_base + lo + ln]
-        to_recv, to_send = apply_action_set(prim, incoming, local, m.dtype)
+        to_recv, to_send = apply_action_set(prim, incoming, local, m.dtype, m.op)
         if to_recv is not None:
             st.recvbuf[recv_base + lo: recv_base + lo + ln] = to_recv
         if to_send is not None:

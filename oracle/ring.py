@@ -17,11 +17,16 @@ its textbook definition; in floating point the reduction ORDER is the ring's:
   BC  out           = x_root
   n = 1             => copy
 
-Indices are mod n.  (+) per dtype (reading R7):
-  i32  : (a + b) mod 2^32
-  f32  : IEEE-754 binary32 add, round-to-nearest-even (numpy float32 +)
-  bf16 : RNE_bf16(float32(a) + float32(b))   (= correctly rounded bf16 sum,
-         double rounding is innocuous since 24 >= 2*8 + 2)
+Indices are mod n.  (+) is the collective's reducing function (PAPER.md:306
+"a specified reducing function"): sum (default), prod, max or min, per dtype
+(readings R7 / R22):
+  i32  : (a + b) mod 2^32, (a * b) mod 2^32, signed max / min
+  f32  : IEEE-754 binary32 add / multiply, round-to-nearest-even (numpy float32)
+  bf16 : RNE_bf16(float32(a) op float32(b))  (= the correctly rounded bf16 result:
+         a bf16 product is exact in f32, and for sums double rounding is innocuous
+         since 24 >= 2*8 + 2)
+  f16  : RNE_f16(float32(a) op float32(b))   (same argument, 24 >= 2*11 + 2)
+  max / min are exact (no rounding); inputs carry no NaN.
 
 Where the paper is silent (segment map, operand order, bf16 partial precision)
 the readings are SURVEY.md §8(c) Q6/Q7, listed in DESIGN.md.
@@ -33,7 +38,8 @@ import numpy as np
 from inputs import hashgen
 
 KINDS = ("allreduce", "allgather", "reducescatter", "broadcast")
-ITEMSIZE = {"i32": 4, "f32": 4, "bf16": 2}
+ITEMSIZE = {"i32": 4, "f32": 4, "bf16": 2, "f16": 2}
+OPS = ("sum", "prod", "max", "min")
 
 
 # ----------------------------------------------------------------------------- (+) per dtype
@@ -48,23 +54,49 @@ def bf16_to_f32(b: np.ndarray) -> np.ndarray:
     return (np.asarray(b, dtype=np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32)
 
 
-def add(a: np.ndarray, b: np.ndarray, dtype: str) -> np.ndarray:
-    """Elementwise reduction function (+) ("reduces data ... with a
-    specified reducing function"; sum only)."""
+def _f32_op(x: np.ndarray, y: np.ndarray, op: str) -> np.ndarray:
+    """The reducing function on float32 operands (IEEE, round to nearest even)."""
+    if op == "sum":
+        return (x + y).astype(np.float32)
+    if op == "prod":
+        return (x * y).astype(np.float32)
+    if op == "max":
+        return np.maximum(x, y)
+    if op == "min":
+        return np.minimum(x, y)
+    raise ValueError(op)
+
+
+def add(a: np.ndarray, b: np.ndarray, dtype: str, op: str = "sum") -> np.ndarray:
+    """Elementwise reducing function (+) ("reduces data ... with a
+    specified reducing function"): sum, prod, max or min."""
     if dtype == "i32":
-        return (np.asarray(a).view(np.uint32) + np.asarray(b).view(np.uint32)).view(np.int32)
+        ua, ub = np.asarray(a).view(np.uint32), np.asarray(b).view(np.uint32)
+        if op == "sum":
+            return (ua + ub).view(np.int32)
+        if op == "prod":
+            return (ua * ub).view(np.int32)            # mod 2^32 (two's complement product)
+        ia, ib = np.asarray(a).view(np.int32), np.asarray(b).view(np.int32)
+        if op == "max":
+            return np.maximum(ia, ib)
+        if op == "min":
+            return np.minimum(ia, ib)
+        raise ValueError(op)
     if dtype == "f32":
-        return (np.asarray(a, dtype=np.float32) + np.asarray(b, dtype=np.float32)).astype(np.float32)
+        return _f32_op(np.asarray(a, dtype=np.float32), np.asarray(b, dtype=np.float32), op)
     if dtype == "bf16":
-        return bf16_rne(bf16_to_f32(a) + bf16_to_f32(b))
+        return bf16_rne(_f32_op(bf16_to_f32(a), bf16_to_f32(b), op))
+    if dtype == "f16":
+        return _f32_op(np.asarray(a, dtype=np.float16).astype(np.float32),
+                       np.asarray(b, dtype=np.float16).astype(np.float32), op).astype(np.float16)
     raise ValueError(dtype)
 
 
-def ring_fold(parts_in_ring_order, dtype: str) -> np.ndarray:
+def ring_fold(parts_in_ring_order, dtype: str, op: str = "sum") -> np.ndarray:
     """Left fold: ((p0 (+) p1) (+) p2) ... -- p0 = x_{c+1}, ..., last = x_c."""
     acc = np.array(parts_in_ring_order[0], copy=True)
     for p in parts_in_ring_order[1:]:
-        acc = add(acc, p, dtype)
+        acc = add(acc, p, dtype, op)
     return acc
 
 
@@ -91,7 +123,7 @@ def ar_owner(i, count: int, n: int, dtype: str):
 
 
 # ----------------------------------------------------------------------------- full results
-def allreduce(xs, dtype: str) -> np.ndarray:
+def allreduce(xs, dtype: str, op: str = "sum") -> np.ndarray:
     """AR result (identical on every rank) for per-rank inputs xs[r] (length N each)."""
     n = len(xs)
     count = len(xs[0])
@@ -103,17 +135,17 @@ def allreduce(xs, dtype: str) -> np.ndarray:
         lo, hi = min(c * L, count), min((c + 1) * L, count)
         if lo >= hi:
             continue
-        out[lo:hi] = ring_fold([xs[q][lo:hi] for q in fold_order(c, n)], dtype)
+        out[lo:hi] = ring_fold([xs[q][lo:hi] for q in fold_order(c, n)], dtype, op)
     return out
 
 
-def reduce_scatter(xs, dtype: str):
+def reduce_scatter(xs, dtype: str, op: str = "sum"):
     """RS: xs[r] has n*N elements; returns [out_0, ..., out_{n-1}], out_r has N."""
     n = len(xs)
     N = len(xs[0]) // n
     if n == 1:
         return [np.array(xs[0][:N], copy=True)]
-    return [ring_fold([xs[q][r * N:(r + 1) * N] for q in fold_order(r, n)], dtype) for r in range(n)]
+    return [ring_fold([xs[q][r * N:(r + 1) * N] for q in fold_order(r, n)], dtype, op) for r in range(n)]
 
 
 def all_gather(xs) -> np.ndarray:
@@ -127,7 +159,7 @@ def broadcast(xs, root: int) -> np.ndarray:
 
 # ----------------------------------------------------------------------------- sampled results
 def expected_at(kind: str, dtype: str, n: int, count: int, seed: int, coll: int,
-                idx, rank: int = 0, root: int = 0) -> np.ndarray:
+                idx, rank: int = 0, root: int = 0, op: str = "sum") -> np.ndarray:
     """Expected output values at output indices ``idx`` of rank ``rank``, computing
     only the needed inputs from the counter-based generator (inputs.hashgen).
 
@@ -152,11 +184,11 @@ def expected_at(kind: str, dtype: str, n: int, count: int, seed: int, coll: int,
         for c in range(n):
             m = owner == c
             if m.any():
-                out[m] = ring_fold([val(q, idx[m]) for q in fold_order(c, n)], dtype)
+                out[m] = ring_fold([val(q, idx[m]) for q in fold_order(c, n)], dtype, op)
         return out
     if kind == "reducescatter":
         src = rank * count + idx
-        return ring_fold([val(q, src) for q in fold_order(rank, n)], dtype)
+        return ring_fold([val(q, src) for q in fold_order(rank, n)], dtype, op)
     raise ValueError(kind)
 
 
@@ -166,14 +198,14 @@ def inputs_full(kind: str, dtype: str, n: int, count: int, seed: int, coll: int)
     return [hashgen.buffer(dtype, seed, coll, r, inlen) for r in range(n)]
 
 
-def result_full(kind: str, dtype: str, xs, root: int = 0):
+def result_full(kind: str, dtype: str, xs, root: int = 0, op: str = "sum"):
     """Per-rank expected outputs for materialised inputs xs."""
     n = len(xs)
     if kind == "allreduce":
-        o = allreduce(xs, dtype)
+        o = allreduce(xs, dtype, op)
         return [o] * n
     if kind == "reducescatter":
-        return reduce_scatter(xs, dtype)
+        return reduce_scatter(xs, dtype, op)
     if kind == "allgather":
         o = all_gather(xs)
         return [o] * n

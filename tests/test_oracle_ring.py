@@ -264,3 +264,108 @@ def test_o1_equals_o2_execution(kind, dtype, n):
         for r in range(n):
             got = sim.results[(r, 0, 0)]
             assert np.array_equal(_bits(got), _bits(exp[r])), (kind, dtype, n, count, r)
+
+
+# ------------------------------------------------------------------ reducing functions and f16
+def _round_to_sig_bits(x: Fraction, bits: int, emin: int):
+    """Exact rational -> nearest binary float with `bits` significand bits (ties to
+    even), subnormals below 2^emin (IEEE gradual underflow)."""
+    if x == 0:
+        return Fraction(0)
+    sign = -1 if x < 0 else 1
+    s = abs(x)
+    e = 0
+    while s >= 2:
+        s /= 2
+        e += 1
+    while s < 1:
+        s *= 2
+        e -= 1
+    e = max(e, emin)                     # subnormal: fixed exponent, fewer bits
+    q = abs(x) / Fraction(2) ** e * 2 ** (bits - 1)
+    fl = q.numerator // q.denominator
+    rem = q - fl
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and fl % 2 == 1):
+        fl += 1
+    return sign * Fraction(fl, 2 ** (bits - 1)) * Fraction(2) ** e
+
+
+@pytest.mark.parametrize("op", ["sum", "prod"])
+def test_f16_ops_correctly_rounded(op):
+    """f16 sum / product equal the exact rational result rounded to binary16
+    (11 significant bits, subnormals below 2^-14) -- an independent derivation."""
+    a = hashgen.values("f16", 3, 0, 0, np.arange(2000))
+    b = hashgen.values("f16", 3, 0, 1, np.arange(2000))
+    got = ring.add(a, b, "f16", op)
+    for x, y, g in zip(a.tolist(), b.tolist(), got.tolist()):
+        fx, fy = Fraction(x), Fraction(y)
+        exact = fx + fy if op == "sum" else fx * fy
+        assert Fraction(g) == _round_to_sig_bits(exact, 11, -14), (x, y, g)
+
+
+def test_bf16_prod_correctly_rounded():
+    a = hashgen.values("bf16", 5, 0, 0, np.arange(2000))
+    b = hashgen.values("bf16", 5, 0, 1, np.arange(2000))
+    got = ring.bf16_to_f32(ring.add(a, b, "bf16", "prod"))
+    for x, y, g in zip(ring.bf16_to_f32(a).tolist(), ring.bf16_to_f32(b).tolist(), got.tolist()):
+        assert Fraction(g) == _round_to_sig_bits(Fraction(x) * Fraction(y), 8, -126)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f16", "i32"])
+@pytest.mark.parametrize("n", [2, 3, 8])
+def test_max_min_are_elementwise_extrema(dtype, n):
+    """max / min need no rounding: the all-reduce equals numpy's element-wise
+    extremum over ranks (order-free), and reduce-scatter its segments."""
+    xs = ring.inputs_full("allreduce", dtype, n, 3001, 8, 2)
+    conv = (lambda v: ring.bf16_to_f32(v)) if dtype == "bf16" else (lambda v: v)
+    for op, f in (("max", np.maximum.reduce), ("min", np.minimum.reduce)):
+        got = conv(ring.allreduce(xs, dtype, op))
+        assert np.array_equal(got, f([conv(x) for x in xs])), op
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_int_prod_closed_form(n):
+    """i32 prod with rank-constant inputs r+1: n! (mod 2^32); wraps at n = 13+."""
+    xs = [np.full(777, r + 1, dtype=np.int32) for r in range(n)]
+    import math
+    assert np.all(ring.allreduce(xs, "i32", "prod") == math.factorial(n))
+    big = [np.full(5, 1 << 20, dtype=np.int32) for _ in range(2)]
+    assert np.all(ring.allreduce(big, "i32", "prod") == 0)          # 2^40 mod 2^32
+
+
+@pytest.mark.parametrize("n", [3, 8])
+def test_fp32_prod_order_is_observable(n):
+    """The ring's fold order matters for products too (rounding): the O1 result
+    differs from a rank-0-first fold on some elements of random inputs."""
+    xs = ring.inputs_full("allreduce", "f32", n, 4096, 6, 6)
+    o = ring.allreduce(xs, "f32", "prod")
+    naive = xs[0].copy()
+    for x in xs[1:]:
+        naive = (naive * x).astype(np.float32)
+    assert (o.view(np.uint32) != naive.view(np.uint32)).sum() > 0
+    assert np.allclose(o, naive, rtol=1e-5, atol=0)
+
+
+@pytest.mark.parametrize("op", ["sum", "prod", "max", "min"])
+@pytest.mark.parametrize("dtype", ["f32", "f16", "i32"])
+def test_o1_equals_o2_execution_ops(op, dtype):
+    """O2 executes the primitive sequences with the same reducing function; its
+    outputs equal O1's closed form bit for bit (AR and RS, n = 3)."""
+    n = 3
+    for kind in ("allreduce", "reducescatter"):
+        meta = dfce.CollMeta(0, kind, dtype, 70, nblocks=2, op=op)
+        cfg = dfce.SimConfig(lanes=2, K=3, slice_elems=8, slices_per_chunk=2, seed=1)
+        sim, bufs = dfce.run_orders([meta], [[0]] * n, cfg, seed=4)
+        xs = [bufs[(r, 0, 0)][0] for r in range(n)]
+        exp = ring.result_full(kind, dtype, xs, op=op)
+        for r in range(n):
+            assert np.array_equal(_bits(sim.results[(r, 0, 0)]), _bits(exp[r])), (kind, r)
+
+
+def test_f16_generator_exact():
+    """f16 inputs are exactly (m - 1024) * 2^(-10-e): no rounding in generation."""
+    v = hashgen.values("f16", 1, 2, 3, np.arange(5000)).astype(np.float64)
+    scaled = [Fraction(x) for x in v.tolist()]
+    for x in scaled:
+        assert x == 0 or any((x * 2 ** (10 + e)).denominator == 1 and abs(x * 2 ** (10 + e)) <= 1024
+                             for e in range(8))
