@@ -27,6 +27,7 @@
 // Connectors are dedicated per (collective, block).
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 #include "occl_internal.h"
@@ -100,29 +101,56 @@ __device__ __forceinline__ T ld_cg_scalar(const T* p) {
   return *reinterpret_cast<const volatile T*>(p);
 }
 
-// ------------------------------------------------------------------ reduction (+)
-// f32: IEEE add, round-to-nearest-even (no FMA contraction: plain __fadd_rn).
-// i32: two's-complement wrap.  bf16: correctly rounded bf16 add (__hadd2).
-template <int DT> __device__ __forceinline__ uint4 vadd(const uint4& a, const uint4& b);
-template <> __device__ __forceinline__ uint4 vadd<kF32>(const uint4& a, const uint4& b) {
-  uint4 r;
-  r.x = __float_as_uint(__fadd_rn(__uint_as_float(a.x), __uint_as_float(b.x)));
-  r.y = __float_as_uint(__fadd_rn(__uint_as_float(a.y), __uint_as_float(b.y)));
-  r.z = __float_as_uint(__fadd_rn(__uint_as_float(a.z), __uint_as_float(b.z)));
-  r.w = __float_as_uint(__fadd_rn(__uint_as_float(a.w), __uint_as_float(b.w)));
-  return r;
+// ------------------------------------------------------------------ reducing function (+)
+// The collective's reducing function, per element, bit-exact with
+// the oracle (R7 / R22): sum / prod / max / min.
+// f32: IEEE add / multiply round-to-nearest-even (__fadd_rn / __fmul_rn: no FMA
+// contraction).  i32: two's-complement wrap, signed max / min.  bf16 / f16: the
+// correctly rounded 16-bit result (__hadd2 / __hmul2 / __hmax2 / __hmin2).
+enum : int { kSum = 0, kProd = 1, kMax = 2, kMin = 3 };
+
+template <int OP> __device__ __forceinline__ uint32_t op_f32(uint32_t a, uint32_t b) {
+  const float x = __uint_as_float(a), y = __uint_as_float(b);
+  if constexpr (OP == kSum) return __float_as_uint(__fadd_rn(x, y));
+  else if constexpr (OP == kProd) return __float_as_uint(__fmul_rn(x, y));
+  else if constexpr (OP == kMax) return __float_as_uint(fmaxf(x, y));
+  else return __float_as_uint(fminf(x, y));
 }
-template <> __device__ __forceinline__ uint4 vadd<kI32>(const uint4& a, const uint4& b) {
-  return make_uint4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+template <int OP> __device__ __forceinline__ uint32_t op_i32(uint32_t a, uint32_t b) {
+  if constexpr (OP == kSum) return a + b;
+  else if constexpr (OP == kProd) return a * b;
+  else if constexpr (OP == kMax) return (uint32_t)max((int32_t)a, (int32_t)b);
+  else return (uint32_t)min((int32_t)a, (int32_t)b);
 }
-__device__ __forceinline__ uint32_t add_bf16x2(uint32_t a, uint32_t b) {
-  __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&a);
-  __nv_bfloat162 y = *reinterpret_cast<__nv_bfloat162*>(&b);
-  __nv_bfloat162 z = __hadd2(x, y);
+template <int OP> __device__ __forceinline__ uint32_t op_bf16x2(uint32_t a, uint32_t b) {
+  const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(&a);
+  const __nv_bfloat162 y = *reinterpret_cast<const __nv_bfloat162*>(&b);
+  __nv_bfloat162 z;
+  if constexpr (OP == kSum) z = __hadd2(x, y);
+  else if constexpr (OP == kProd) z = __hmul2(x, y);
+  else if constexpr (OP == kMax) z = __hmax2(x, y);
+  else z = __hmin2(x, y);
   return *reinterpret_cast<uint32_t*>(&z);
 }
-template <> __device__ __forceinline__ uint4 vadd<kBF16>(const uint4& a, const uint4& b) {
-  return make_uint4(add_bf16x2(a.x, b.x), add_bf16x2(a.y, b.y), add_bf16x2(a.z, b.z), add_bf16x2(a.w, b.w));
+template <int OP> __device__ __forceinline__ uint32_t op_f16x2(uint32_t a, uint32_t b) {
+  const __half2 x = *reinterpret_cast<const __half2*>(&a);
+  const __half2 y = *reinterpret_cast<const __half2*>(&b);
+  __half2 z;
+  if constexpr (OP == kSum) z = __hadd2(x, y);
+  else if constexpr (OP == kProd) z = __hmul2(x, y);
+  else if constexpr (OP == kMax) z = __hmax2(x, y);
+  else z = __hmin2(x, y);
+  return *reinterpret_cast<uint32_t*>(&z);
+}
+// one 32-bit lane of packed elements
+template <int DT, int OP> __device__ __forceinline__ uint32_t op_w(uint32_t a, uint32_t b) {
+  if constexpr (DT == kF32) return op_f32<OP>(a, b);
+  else if constexpr (DT == kI32) return op_i32<OP>(a, b);
+  else if constexpr (DT == kBF16) return op_bf16x2<OP>(a, b);
+  else return op_f16x2<OP>(a, b);
+}
+template <int DT, int OP> __device__ __forceinline__ uint4 vop(const uint4& a, const uint4& b) {
+  return make_uint4(op_w<DT, OP>(a.x, b.x), op_w<DT, OP>(a.y, b.y), op_w<DT, OP>(a.z, b.z), op_w<DT, OP>(a.w, b.w));
 }
 
 // ------------------------------------------------------------------ primitives
@@ -153,22 +181,23 @@ struct SliceDesc {
   int64_t nelem;
   int prim;
   int dtype;
+  int op;              // reducing function (kSum / kProd / kMax / kMin)
 };
 
 template <int DT> struct Elem;
-template <> struct Elem<kF32> { typedef float T; };
-template <> struct Elem<kI32> { typedef int32_t T; };
+template <> struct Elem<kF32> { typedef uint32_t T; };
+template <> struct Elem<kI32> { typedef uint32_t T; };
 template <> struct Elem<kBF16> { typedef uint16_t T; };
+template <> struct Elem<kF16> { typedef uint16_t T; };
 
-template <int DT>
-__device__ __forceinline__ typename Elem<DT>::T sadd(typename Elem<DT>::T a, typename Elem<DT>::T b);
-template <> __device__ __forceinline__ float sadd<kF32>(float a, float b) { return __fadd_rn(a, b); }
-template <> __device__ __forceinline__ int32_t sadd<kI32>(int32_t a, int32_t b) {
-  return (int32_t)((uint32_t)a + (uint32_t)b);
-}
-template <> __device__ __forceinline__ uint16_t sadd<kBF16>(uint16_t a, uint16_t b) {
-  __nv_bfloat16 x = __ushort_as_bfloat16(a), y = __ushort_as_bfloat16(b);
-  return __bfloat16_as_ushort(__hadd(x, y));
+// one element (bit pattern) of the reducing function
+template <int DT, int OP>
+__device__ __forceinline__ typename Elem<DT>::T sop(typename Elem<DT>::T a, typename Elem<DT>::T b) {
+  if constexpr (sizeof(typename Elem<DT>::T) == 4) {
+    return op_w<DT, OP>(a, b);
+  } else {
+    return (typename Elem<DT>::T)(op_w<DT, OP>((uint32_t)a, (uint32_t)b) & 0xffffu);   // low half only
+  }
 }
 
 // Move one slice with the data warps: 128-bit vectors, U independent loads in
@@ -176,7 +205,7 @@ template <> __device__ __forceinline__ uint16_t sadd<kBF16>(uint16_t a, uint16_t
 // Loads bypass L1 (ld.global.cg): connector slots are rewritten by peers and the
 // persistent kernel must never see a stale line.  The action bits are
 // warp-uniform runtime flags; only the element type is a template.
-template <int DT>
+template <int DT, int OP>
 __device__ __forceinline__ void move_slice(const int prim, const char* src, const char* cin, char* dst, char* cout,
                                            const int64_t nelem, const int tid, const int nt) {
   typedef typename Elem<DT>::T T;
@@ -202,7 +231,7 @@ __device__ __forceinline__ void move_slice(const int prim, const char* src, cons
 #pragma unroll
       for (int u = 0; u < U; ++u) c[u] = __ldcg(vs + i + u * nt);
 #pragma unroll
-      for (int u = 0; u < U; ++u) a[u] = vadd<DT>(a[u], c[u]);
+      for (int u = 0; u < U; ++u) a[u] = vop<DT, OP>(a[u], c[u]);
     }
     if (copy) {
 #pragma unroll
@@ -216,7 +245,7 @@ __device__ __forceinline__ void move_slice(const int prim, const char* src, cons
   // remaining vectors, one per thread per iteration
   for (; i < nvec; i += nt) {
     uint4 v = __ldcg(vi + i);
-    if (reduce) v = vadd<DT>(v, __ldcg(vs + i));
+    if (reduce) v = vop<DT, OP>(v, __ldcg(vs + i));
     if (copy) __stcg(vd + i, v);
     if (send) __stcg(vo + i, v);
   }
@@ -226,8 +255,8 @@ __device__ __forceinline__ void move_slice(const int prim, const char* src, cons
   T* sd = reinterpret_cast<T*>(dst);
   T* so = reinterpret_cast<T*>(cout);
   for (int e = nvec * A + tid; e < n; e += nt) {
-    T v = __ldcg(si + e);
-    if (reduce) v = sadd<DT>(v, __ldcg(ss + e));
+    T v = ld_cg_scalar(si + e);
+    if (reduce) v = sop<DT, OP>(v, ld_cg_scalar(ss + e));
     if (copy) sd[e] = v;
     if (send) so[e] = v;
   }
@@ -286,7 +315,7 @@ __device__ __forceinline__ int directify(int prim, int kind, int n, int step, bo
   return prim;
 }
 
-__device__ __forceinline__ int elem_size(int dt) { return dt == kBF16 ? 2 : 4; }
+__device__ __forceinline__ int elem_size(int dt) { return (dt == kBF16 || dt == kF16) ? 2 : 4; }
 
 // Segment q's base offsets (elements) in the send / recv buffers and length.
 __device__ __forceinline__ void seg_geom(int kind, int n, int r, uint64_t count, uint64_t segLen, int q,
@@ -440,6 +469,7 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched
   ns->root = e.root; ns->nblocks = e.nblocks; ns->nsteps = (uint16_t)nsteps; ns->priority = e.priority;
   ns->lane = (uint32_t)lane;
   ns->sub = e.sub;
+  ns->op = e.op;
   ns->proto = ll;
   ns->spc = (uint32_t)spc;
   uint4* dst = reinterpret_cast<uint4*>(g);
@@ -836,6 +866,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
       }
       sd.prim = curPrim;
       sd.dtype = dtype;
+      sd.op = (int)cx.op;
       sd.headOut = headOut;
       sd.creditOut = creditOut;
       sd.headVal = di.nsent + 1;
@@ -1018,7 +1049,7 @@ __device__ __forceinline__ uint4 lds_v4(const void* p) {
 // compute warps move it with register loads (move_slice).
 __device__ __forceinline__ int tma_vec_bytes(int dtype, int64_t nelem, const char* src, const char* dst,
                                              const char* cout) {
-  const int isz = dtype == kBF16 ? 2 : 4;
+  const int isz = (dtype == kBF16 || dtype == kF16) ? 2 : 4;
   if (nelem <= 0) return 0;
   if ((((uintptr_t)src) | ((uintptr_t)dst) | ((uintptr_t)cout)) & 15) return 0;   // cout: a peer buffer (direct)
   const int vb = (int)((nelem * isz) & ~(int64_t)15);
@@ -1068,7 +1099,7 @@ __device__ __noinline__ void producer_main(const DaemonParams& p, Pipe& pipe, St
 
 // Compute warps: reduce / copy the staged tiles into the recv buffer and the
 // downstream connector with 128-bit stores.
-template <int DT>
+template <int DT, int OP>
 __device__ __forceinline__ void consume_tile(const int prim, char* dst, char* cout, const Stage& s, int sz, int tid,
                                              int nt, bool hints, uint64_t pol) {
   const bool reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
@@ -1077,7 +1108,7 @@ __device__ __forceinline__ void consume_tile(const int prim, char* dst, char* co
   const int nv = sz >> 4;
   for (int i = tid; i < nv; i += nt) {
     uint4 v = lds_v4(&s.in[i]);
-    if (reduce) v = vadd<DT>(v, lds_v4(&s.loc[i]));
+    if (reduce) v = vop<DT, OP>(v, lds_v4(&s.loc[i]));
     if (copy) {
       if (hints) st_cg_hint(vd + i, v, pol);
       else __stcg(vd + i, v);
@@ -1092,7 +1123,7 @@ __device__ __forceinline__ void consume_tile(const int prim, char* dst, char* co
 // sender no release fence -- a line is valid once both flags match.  Used for
 // latency-bound collectives (small per-block parts).  Payload = the slice's
 // elements packed 8 B per line; reduction per element as in the Simple path.
-template <int DT>
+template <int DT, int OP>
 __device__ __forceinline__ void ll_slice(const int prim, const char* src, const char* cin, char* dst, char* cout,
                                          const int64_t nelem, const uint32_t inSeq, const uint32_t outSeq,
                                          const int tid, const int nt) {
@@ -1118,12 +1149,12 @@ __device__ __forceinline__ void ll_slice(const int prim, const char* src, const 
       if (reduce) {
 #pragma unroll
         for (int k = 0; k < PER; ++k)
-          if (e0 + k < nelem) pay.e[k] = sadd<DT>(pay.e[k], __ldcg(s + e0 + k));
+          if (e0 + k < nelem) pay.e[k] = sop<DT, OP>(pay.e[k], ld_cg_scalar(s + e0 + k));
       }
     } else {
 #pragma unroll
       for (int k = 0; k < PER; ++k)
-        if (e0 + k < nelem) pay.e[k] = __ldcg(s + e0 + k);
+        if (e0 + k < nelem) pay.e[k] = ld_cg_scalar(s + e0 + k);
     }
     if (copy) {
 #pragma unroll
@@ -1139,15 +1170,55 @@ __device__ __forceinline__ void ll_slice(const int prim, const char* src, const 
 // Compute warps: every compute warp takes part in every slice, in order.  The
 // descriptor is read field by field into registers (a struct copy would live in
 // local memory and be re-read in the inner loop).
-template <int DT>
+template <int DT, int OP>
 __device__ __forceinline__ void reduce_tile_smem(Stage& st, int sz, int tid, int nt) {
   const int nv = sz >> 4;
   for (int i = tid; i < nv; i += nt) {
-    const uint4 v = vadd<DT>(lds_v4(&st.in[i]), lds_v4(&st.loc[i]));
+    const uint4 v = vop<DT, OP>(lds_v4(&st.in[i]), lds_v4(&st.loc[i]));
     asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" :: "r"(smem_u32(&st.in[i])), "r"(v.x), "r"(v.y), "r"(v.z),
                  "r"(v.w) : "memory");
   }
 }
+
+// ragged tail (< 16 B) of a TMA-path slice, straight from global memory
+template <int DT, int OP>
+__device__ __forceinline__ void tail_slice(const int prim, const char* src, const char* cin, char* dst, char* cout,
+                                           int64_t e0, int64_t nelem, int tid, int nt) {
+  typedef typename Elem<DT>::T T;
+  const bool rv = prim & A_RECV, rd = prim & A_REDUCE;
+  const T* si = reinterpret_cast<const T*>(rv ? cin : src);
+  const T* ss = reinterpret_cast<const T*>(src);
+  for (int64_t e = e0 + tid; e < nelem; e += nt) {
+    T v = ld_cg_scalar(si + e);
+    if (rd) v = sop<DT, OP>(v, ld_cg_scalar(ss + e));
+    if (prim & A_COPY) reinterpret_cast<T*>(dst)[e] = v;
+    if (prim & A_SEND) reinterpret_cast<T*>(cout)[e] = v;
+  }
+}
+
+// Instantiate FN<dtype, op>(args...) for the slice's runtime (dtype, op); copy-only
+// slices use the element size alone (op irrelevant).
+#define OCCL_DISPATCH(dtype, op, FN, ...)                                          \
+  do {                                                                             \
+    switch ((dtype) * 4 + (op)) {                                                  \
+      case kI32 * 4 + kSum: FN<kI32, kSum>(__VA_ARGS__); break;                    \
+      case kI32 * 4 + kProd: FN<kI32, kProd>(__VA_ARGS__); break;                  \
+      case kI32 * 4 + kMax: FN<kI32, kMax>(__VA_ARGS__); break;                    \
+      case kI32 * 4 + kMin: FN<kI32, kMin>(__VA_ARGS__); break;                    \
+      case kF32 * 4 + kSum: FN<kF32, kSum>(__VA_ARGS__); break;                    \
+      case kF32 * 4 + kProd: FN<kF32, kProd>(__VA_ARGS__); break;                  \
+      case kF32 * 4 + kMax: FN<kF32, kMax>(__VA_ARGS__); break;                    \
+      case kF32 * 4 + kMin: FN<kF32, kMin>(__VA_ARGS__); break;                    \
+      case kBF16 * 4 + kSum: FN<kBF16, kSum>(__VA_ARGS__); break;                  \
+      case kBF16 * 4 + kProd: FN<kBF16, kProd>(__VA_ARGS__); break;                \
+      case kBF16 * 4 + kMax: FN<kBF16, kMax>(__VA_ARGS__); break;                  \
+      case kBF16 * 4 + kMin: FN<kBF16, kMin>(__VA_ARGS__); break;                  \
+      case kF16 * 4 + kSum: FN<kF16, kSum>(__VA_ARGS__); break;                    \
+      case kF16 * 4 + kProd: FN<kF16, kProd>(__VA_ARGS__); break;                  \
+      case kF16 * 4 + kMax: FN<kF16, kMax>(__VA_ARGS__); break;                    \
+      default: FN<kF16, kMin>(__VA_ARGS__); break;                                 \
+    }                                                                              \
+  } while (0)
 
 __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pipe, Stage* stages, uint64_t* tfull,
                                           uint64_t* tempty, uint64_t* tred, const int ctid, const int cnt) {
@@ -1174,17 +1245,14 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
     char* cout = dp->cout;
     const long long t1 = clock64();
     const int vb = tma_vec_bytes(dtype, nelem, src, dst, cout);
+    const int op = dp->op;
     if (prim & A_LL) {
       const uint32_t inSeq = (uint32_t)dp->creditVal, outSeq = (uint32_t)dp->headVal;
-      if (dtype == kBF16) ll_slice<kBF16>(prim, src, cin, dst, cout, nelem, inSeq, outSeq, ctid, cnt);
-      else if (dtype == kF32) ll_slice<kF32>(prim, src, cin, dst, cout, nelem, inSeq, outSeq, ctid, cnt);
-      else ll_slice<kI32>(prim, src, cin, dst, cout, nelem, inSeq, outSeq, ctid, cnt);
+      OCCL_DISPATCH(dtype, op, ll_slice, prim, src, cin, dst, cout, nelem, inSeq, outSeq, ctid, cnt);
     } else if (!(prim & (A_COPY | A_SEND))) {
       // direct final receive: the data is already in place, nothing to move
     } else if (vb == 0) {                              // small or misaligned: register path
-      if (dtype == kBF16) move_slice<kBF16>(prim, src, cin, dst, cout, nelem, ctid, cnt);
-      else if (dtype == kF32) move_slice<kF32>(prim, src, cin, dst, cout, nelem, ctid, cnt);
-      else move_slice<kI32>(prim, src, cin, dst, cout, nelem, ctid, cnt);
+      OCCL_DISPATCH(dtype, op, move_slice, prim, src, cin, dst, cout, nelem, ctid, cnt);
     } else {
       const bool disc = discard && (prim & A_RECV) && !(prim & A_DIN) && !((uintptr_t)cin & 127);
       for (int off = 0; off < vb; off += kTile) {
@@ -1197,9 +1265,7 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
           // bulk-store mode: reduce in place in shared memory; the publisher lane
           // stores the tile with cp.async.bulk (copy tiles need no compute at all)
           if (prim & A_REDUCE) {
-            if (dtype == kF32) reduce_tile_smem<kF32>(stages[s], sz, ctid, cnt);
-            else if (dtype == kBF16) reduce_tile_smem<kBF16>(stages[s], sz, ctid, cnt);
-            else reduce_tile_smem<kI32>(stages[s], sz, ctid, cnt);
+            OCCL_DISPATCH(dtype, op, reduce_tile_smem, stages[s], sz, ctid, cnt);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> async proxy
           }
           // every tile (copy tiles too) completes one tred phase, so tred[s] stays
@@ -1209,35 +1275,16 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
           continue;
         }
         if (prim & A_REDUCE) {
-          if (dtype == kF32) consume_tile<kF32>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol);
-          else if (dtype == kBF16) consume_tile<kBF16>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol);
-          else consume_tile<kI32>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol);
+          OCCL_DISPATCH(dtype, op, consume_tile, prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol);
         } else {
-          consume_tile<kI32>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol);
+          consume_tile<kI32, kSum>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol);   // copy only
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[s]);
       }
       // ragged tail (< 16 B) straight from global memory
-      const int isz = dtype == kBF16 ? 2 : 4;
-      const int64_t e0 = vb / isz;
-      const bool rv = prim & A_RECV, rd = prim & A_REDUCE;
-      for (int64_t e = e0 + ctid; e < nelem; e += cnt) {
-        if (isz == 2) {
-          uint16_t v = __ldcg(reinterpret_cast<const uint16_t*>(rv ? cin : src) + e);
-          if (rd) v = sadd<kBF16>(v, __ldcg(reinterpret_cast<const uint16_t*>(src) + e));
-          if (prim & A_COPY) reinterpret_cast<uint16_t*>(dst)[e] = v;
-          if (prim & A_SEND) reinterpret_cast<uint16_t*>(cout)[e] = v;
-        } else {
-          uint32_t v = __ldcg(reinterpret_cast<const uint32_t*>(rv ? cin : src) + e);
-          if (rd) {
-            const uint32_t w = __ldcg(reinterpret_cast<const uint32_t*>(src) + e);
-            v = dtype == kF32 ? __float_as_uint(__fadd_rn(__uint_as_float(v), __uint_as_float(w))) : v + w;
-          }
-          if (prim & A_COPY) reinterpret_cast<uint32_t*>(dst)[e] = v;
-          if (prim & A_SEND) reinterpret_cast<uint32_t*>(cout)[e] = v;
-        }
-      }
+      const int64_t e0 = vb / elem_size(dtype);
+      if (e0 < nelem) OCCL_DISPATCH(dtype, op, tail_slice, prim, src, cin, dst, cout, e0, nelem, ctid, cnt);
     }
     // this warp's stores (ordered by __syncwarp) are released to the publisher,
     // which fences once and raises the peers' flags (publisher_main)

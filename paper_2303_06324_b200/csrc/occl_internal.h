@@ -7,7 +7,7 @@
 namespace occl {
 
 enum Kind : uint16_t { kAllReduce = 0, kAllGather = 1, kReduceScatter = 2, kBroadcast = 3, kExit = 15 };
-enum Dtype : uint16_t { kI32 = 0, kF32 = 1, kBF16 = 2 };
+enum Dtype : uint16_t { kI32 = 0, kF32 = 1, kBF16 = 2, kF16 = 3 };
 
 constexpr int kMaxRanks = 64;
 constexpr int kFlagStride = 384;        // per (coll, block): head @+0, credit @+128, direct @+256 (own lines)
@@ -84,7 +84,8 @@ struct alignas(16) CtxSlot {
   uint32_t sub;        // ring (RingDesc index) of the collective
   uint32_t proto;      // 0 = Simple (TMA slices, head/credit flags), 1 = LL (flags inside the data)
   uint32_t spc;        // slices per chunk of this collective: min(cfg, slices a block's part needs)
-  uint32_t pad[3];
+  uint32_t op;         // reducing function (occlRedOp_t)
+  uint32_t pad[2];
 };
 static_assert(sizeof(CtxSlot) == kCtxBytes, "CtxSlot must be 128 B");
 

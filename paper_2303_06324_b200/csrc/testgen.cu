@@ -6,8 +6,10 @@
 //   u = splitmix64(seed ^ (coll << 40) ^ (rank << 32) ^ i)
 //   f32 : (int(u >> 40) - 2^23) * 2^(-23 - ((u >> 32) & 7))
 //   bf16: (int(u >> 56) - 128)  * 2^(-7  - ((u >> 32) & 7))   (exact, top 16 bits)
+//   f16 : (int(u >> 53) - 1024) * 2^(-10 - ((u >> 32) & 7))  (exact in binary16)
 //   i32 : low 32 bits of u
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 namespace {
@@ -28,10 +30,13 @@ __global__ void fill_kernel(void* dst, uint64_t count, int dtype, uint64_t base,
     } else if (dtype == 1) {
       const int m = (int)(u >> 40) - (1 << 23);
       reinterpret_cast<float*>(dst)[i] = ldexpf((float)m, -23 - e);
-    } else {
+    } else if (dtype == 2) {
       const int m = (int)(u >> 56) - 128;
       const float f = ldexpf((float)m, -7 - e);
       reinterpret_cast<uint16_t*>(dst)[i] = (uint16_t)(__float_as_uint(f) >> 16);
+    } else {
+      const int m = (int)(u >> 53) - 1024;
+      reinterpret_cast<__half*>(dst)[i] = __float2half_rn(ldexpf((float)m, -10 - e));   // exact
     }
   }
 }

@@ -15,8 +15,8 @@ import torch
 
 from . import occl
 
-TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32}
-ITEM = {"f32": 4, "bf16": 2, "i32": 4}
+TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32, "f16": torch.float16}
+ITEM = {"f32": 4, "bf16": 2, "i32": 4, "f16": 2}
 
 
 def ring(nranks, device=0, dist=None, world=1, prank=0, **cfg):

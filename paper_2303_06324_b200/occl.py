@@ -22,11 +22,12 @@ GEN_PATH = os.path.join(_HERE, "lib", "libocclgen.so")
 occlSuccess, occlInvalidArgument, occlInvalidUsage, occlRegistryFull, occlQueueFull, \
     occlDuplicateSubmit, occlUnknownId, occlCudaError, occlSystemError, occlTimeout, \
     occlInProgress, occlInternalError = range(12)
-occlInt32, occlFloat32, occlBfloat16 = 0, 1, 2
-occlSum = 0
+occlInt32, occlFloat32, occlBfloat16, occlFloat16 = 0, 1, 2, 3
+occlSum, occlProd, occlMax, occlMin = 0, 1, 2, 3
+OPS = {"sum": occlSum, "prod": occlProd, "max": occlMax, "min": occlMin}
 occlOrderFifo, occlOrderPriority = 0, 1
 KIND = {"allreduce": 0, "allgather": 1, "reducescatter": 2, "broadcast": 3}
-DTYPE = {"i32": occlInt32, "f32": occlFloat32, "bf16": occlBfloat16}
+DTYPE = {"i32": occlInt32, "f32": occlFloat32, "bf16": occlBfloat16, "f16": occlFloat16}
 OCCL_HANDLE_BYTES = 256
 
 EXPORTED = [
@@ -251,20 +252,20 @@ class Comm:
         self._callbacks = {}
 
     # submission (asynchronous) -------------------------------------------------
-    def all_reduce(self, send, recv, coll_id, count=None, dtype=None):
+    def all_reduce(self, send, recv, coll_id, count=None, dtype=None, op="sum"):
         count = send.numel() if count is None else count
         dtype = _dt(send) if dtype is None else dtype
-        check(occlAllReduce(_ptr(send), _ptr(recv), count, dtype, occlSum, coll_id, self.h), "occlAllReduce")
+        check(occlAllReduce(_ptr(send), _ptr(recv), count, dtype, OPS.get(op, op), coll_id, self.h), "occlAllReduce")
 
     def all_gather(self, send, recv, coll_id, count=None, dtype=None):
         count = send.numel() if count is None else count
         dtype = _dt(send) if dtype is None else dtype
         check(occlAllGather(_ptr(send), _ptr(recv), count, dtype, coll_id, self.h), "occlAllGather")
 
-    def reduce_scatter(self, send, recv, coll_id, count=None, dtype=None):
+    def reduce_scatter(self, send, recv, coll_id, count=None, dtype=None, op="sum"):
         count = recv.numel() if count is None else count
         dtype = _dt(recv) if dtype is None else dtype
-        check(occlReduceScatter(_ptr(send), _ptr(recv), count, dtype, occlSum, coll_id, self.h),
+        check(occlReduceScatter(_ptr(send), _ptr(recv), count, dtype, OPS.get(op, op), coll_id, self.h),
               "occlReduceScatter")
 
     def broadcast(self, send, recv, root, coll_id, count=None, dtype=None):
@@ -272,15 +273,16 @@ class Comm:
         dtype = _dt(recv) if dtype is None else dtype
         check(occlBroadcast(_ptr(send), _ptr(recv), count, dtype, root, coll_id, self.h), "occlBroadcast")
 
-    def submit(self, kind, send, recv, coll_id, count, dtype, root=0):
+    def submit(self, kind, send, recv, coll_id, count, dtype, root=0, op="sum"):
         k = KIND[kind] if isinstance(kind, str) else kind
         d = DTYPE[dtype] if isinstance(dtype, str) else dtype
+        o = OPS[op] if isinstance(op, str) else op
         if k == 0:
-            r = occlAllReduce(_ptr(send), _ptr(recv), count, d, occlSum, coll_id, self.h)
+            r = occlAllReduce(_ptr(send), _ptr(recv), count, d, o, coll_id, self.h)
         elif k == 1:
             r = occlAllGather(_ptr(send), _ptr(recv), count, d, coll_id, self.h)
         elif k == 2:
-            r = occlReduceScatter(_ptr(send), _ptr(recv), count, d, occlSum, coll_id, self.h)
+            r = occlReduceScatter(_ptr(send), _ptr(recv), count, d, o, coll_id, self.h)
         else:
             r = occlBroadcast(_ptr(send), _ptr(recv), count, d, root, coll_id, self.h)
         check(r, f"submit {kind}")
@@ -368,7 +370,8 @@ class Comm:
 
 def _dt(t):
     import torch
-    return {torch.float32: occlFloat32, torch.bfloat16: occlBfloat16, torch.int32: occlInt32}[t.dtype]
+    return {torch.float32: occlFloat32, torch.bfloat16: occlBfloat16, torch.int32: occlInt32,
+            torch.float16: occlFloat16}[t.dtype]
 
 
 def occlCommFuse(comms):

@@ -9,7 +9,7 @@ from inputs import hashgen
 from oracle import ring
 from paper_2303_06324_b200 import occl
 
-TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32}
+TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32, "f16": torch.float16}
 WAIT_S = 60.0
 
 
@@ -20,7 +20,7 @@ def bits(a):
 
 def to_np_bits(t: torch.Tensor) -> np.ndarray:
     t = t.detach().cpu()
-    if t.dtype == torch.bfloat16:
+    if t.dtype in (torch.bfloat16, torch.float16):
         return t.view(torch.int16).numpy().view(np.uint16)
     if t.dtype == torch.float32:
         return t.numpy().view(np.uint32)
@@ -60,7 +60,8 @@ def make_bufs(kind, dtype, n, count, seed, coll, device=0, inplace=False):
             s = torch.empty(in_len(kind, n, count), dtype=TORCH_DT[dtype], device=device)
             occl.test_fill(s, dtype, seed, coll, r)
             rv = torch.full((out_len(kind, n, count),), -7, dtype=TORCH_DT[dtype], device=device) \
-                if dtype != "bf16" else torch.zeros(out_len(kind, n, count), dtype=torch.bfloat16, device=device)
+                if dtype not in ("bf16", "f16") else torch.zeros(out_len(kind, n, count), dtype=TORCH_DT[dtype],
+                                                                device=device)
             sends.append(s)
             recvs.append(rv)
     # inputs complete before submission (occl.h conventions): sync torch's stream
@@ -70,13 +71,13 @@ def make_bufs(kind, dtype, n, count, seed, coll, device=0, inplace=False):
     return sends, recvs
 
 
-def expected_full(kind, dtype, n, count, seed, coll, root=0):
+def expected_full(kind, dtype, n, count, seed, coll, root=0, op="sum"):
     xs = ring.inputs_full(kind, dtype, n, count, seed, coll)
-    return [bits(o) for o in ring.result_full(kind, dtype, xs, root=root)]
+    return [bits(o) for o in ring.result_full(kind, dtype, xs, root=root, op=op)]
 
 
-def check_full(kind, dtype, n, count, seed, coll, recvs, root=0):
-    exp = expected_full(kind, dtype, n, count, seed, coll, root)
+def check_full(kind, dtype, n, count, seed, coll, recvs, root=0, op="sum"):
+    exp = expected_full(kind, dtype, n, count, seed, coll, root, op)
     for r in range(n):
         got = to_np_bits(recvs[r])
         if not np.array_equal(got, exp[r]):
@@ -85,7 +86,7 @@ def check_full(kind, dtype, n, count, seed, coll, recvs, root=0):
                                  f"first at {bad[:8].tolist()} got {got[bad[:4]].tolist()} exp {exp[r][bad[:4]].tolist()}")
 
 
-def check_sampled(kind, dtype, n, count, seed, coll, recvs, root=0, nsamples=4096, boundaries=()):
+def check_sampled(kind, dtype, n, count, seed, coll, recvs, root=0, nsamples=4096, boundaries=(), op="sum"):
     """Sampled comparison at full sizes: random indices + segment/block boundaries."""
     rng = np.random.default_rng(seed ^ coll)
     for r in range(n):
@@ -94,16 +95,16 @@ def check_sampled(kind, dtype, n, count, seed, coll, recvs, root=0, nsamples=409
                               np.array([b for b in boundaries if 0 <= b < L], dtype=np.int64)])
         idx = np.unique(idx)
         got = to_np_bits(recvs[r][torch.from_numpy(idx).to(recvs[r].device)])
-        exp = bits(ring.expected_at(kind, dtype, n, count, seed, coll, idx, rank=r, root=root))
+        exp = bits(ring.expected_at(kind, dtype, n, count, seed, coll, idx, rank=r, root=root, op=op))
         if not np.array_equal(got, exp):
             bad = np.nonzero(got != exp)[0]
             raise AssertionError(f"{kind} {dtype} n={n} count={count} rank {r}: {len(bad)} sampled mismatches "
                                  f"at {idx[bad[:8]].tolist()}")
 
 
-def run_collective(comms, kind, sends, recvs, coll, count, dtype, root=0, order=None):
+def run_collective(comms, kind, sends, recvs, coll, count, dtype, root=0, order=None, op="sum"):
     order = order if order is not None else range(len(comms))
     for r in order:
-        comms[r].submit(kind, sends[r], recvs[r], coll, count, dtype, root)
+        comms[r].submit(kind, sends[r], recvs[r], coll, count, dtype, root, op=op)
     for c in comms:
         c.wait(coll, WAIT_S)

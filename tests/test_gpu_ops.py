@@ -1,0 +1,85 @@
+"""GPU parity for the reducing functions (sum / prod / max / min)
+and fp16, through the C-ABI, bit-exact against the oracle O1 on the same seeded
+inputs: the register path and LL (small configuration) and the TMA staging path
+with direct mode (bench configuration)."""
+import numpy as np
+import pytest
+import torch
+
+from inputs import hashgen
+
+pytestmark = pytest.mark.gpu
+
+import gpu_util as U  # noqa: E402
+
+OPS = ["sum", "prod", "max", "min"]
+DTYPES = ["f32", "bf16", "f16", "i32"]
+
+
+@pytest.fixture(scope="module")
+def occl_mod():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA GPU required for -m gpu tests")
+    from paper_2303_06324_b200 import occl
+    occl._lib()
+    return occl
+
+
+@pytest.fixture(scope="module")
+def rings(occl_mod):
+    made = {}
+
+    def get(n, big):
+        key = (n, big)
+        if key not in made:
+            cfg = dict(gridBlocks=18, sliceBytes=192 << 10, stagingTiles=5, maxColl=64) if big else \
+                dict(gridBlocks=4, sliceBytes=8192, connSlots=3, slicesPerChunk=2, minBlockBytes=16384, maxColl=64)
+            made[key] = occl_mod.local_group(n, 0, **cfg)
+        return made[key]
+    yield get
+    for comms in made.values():
+        occl_mod.destroy_group(comms)
+
+
+def test_f16_generator_matches_numpy(occl_mod):
+    t = torch.empty(70_001, dtype=torch.float16, device=0)
+    occl_mod.test_fill(t, "f16", 0x55, 3, 2, offset=9)
+    torch.cuda.synchronize()
+    exp = hashgen.values("f16", 0x55, 3, 2, np.arange(9, 9 + 70_001)).view(np.uint16)
+    assert np.array_equal(U.to_np_bits(t), exp)
+
+
+@pytest.mark.parametrize("op", OPS)
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("n", [2, 3, 8])
+def test_ops_small(rings, op, dtype, n):
+    comms = rings(n, False)
+    for ci, (kind, count) in enumerate([("allreduce", 1), ("allreduce", 1003), ("allreduce", 70_001),
+                                        ("reducescatter", 777), ("reducescatter", 20_003)]):
+        cid = ci
+        seed = 900 + ci + 10 * OPS.index(op)
+        sends, recvs = U.make_bufs(kind, dtype, n, count, seed, cid)
+        U.run_collective(comms, kind, sends, recvs, cid, count, dtype, op=op)
+        U.check_full(kind, dtype, n, count, seed, cid, recvs, op=op)
+
+
+@pytest.mark.parametrize("op", OPS)
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_ops_bench_config(rings, op, dtype):
+    """TMA staging path (192 KiB slices), 8 ranks, ragged sizes."""
+    comms = rings(8, True)
+    for ci, (kind, count) in enumerate([("allreduce", 1_500_007), ("reducescatter", 200_003)]):
+        seed = 1900 + ci + 10 * OPS.index(op)
+        sends, recvs = U.make_bufs(kind, dtype, 8, count, seed, 20 + ci)
+        U.run_collective(comms, kind, sends, recvs, 20 + ci, count, dtype, op=op)
+        U.check_full(kind, dtype, 8, count, seed, 20 + ci, recvs, op=op)
+
+
+@pytest.mark.parametrize("kind", ["allgather", "broadcast"])
+def test_f16_copies(rings, kind):
+    for big in (False, True):
+        comms = rings(8, big)
+        count = 300_001 if big else 5_003
+        sends, recvs = U.make_bufs(kind, "f16", 8, count, 77, 30)
+        U.run_collective(comms, kind, sends, recvs, 30, count, "f16", root=5)
+        U.check_full(kind, "f16", 8, count, 77, 30, recvs, root=5)
