@@ -230,6 +230,10 @@ occlResult_t occlReduceScatter(const void* sendbuff, void* recvbuff, size_t recv
                                occlDataType_t datatype, occlRedOp_t op, int collId, occlComm_t comm);
 occlResult_t occlBroadcast(const void* sendbuff, void* recvbuff, size_t count,
                            occlDataType_t datatype, int root, int collId, occlComm_t comm);
+/* Reduce to `root` (NCCL ring Reduce: the chain root+1 -> ... -> root folds the
+ * inputs in that order); only the root's recvbuff is written. */
+occlResult_t occlReduce(const void* sendbuff, void* recvbuff, size_t count, occlDataType_t datatype,
+                        occlRedOp_t op, int root, int collId, occlComm_t comm);
 
 /* Block until the latest submission of collId completed locally (its CQE was
  * posted).  timeoutNs < 0 waits forever.  occlUnknownId if never submitted. */
@@ -274,7 +278,8 @@ occlResult_t occlCommSetAutoLaunch(occlComm_t comm, int enable);
 occlResult_t occlCommQuiesce(occlComm_t comm, int64_t timeoutNs);
 /* The CUDA stream (cudaStream_t) the daemon kernel is launched on. */
 occlResult_t occlCommGetStream(occlComm_t comm, void** stream);
-/* Number of blocks a collective of this shape uses (identical on every rank). */
+/* Number of blocks a collective of this shape uses (identical on every rank);
+ * kind: 0 all-reduce, 1 all-gather, 2 reduce-scatter, 3 broadcast, 4 reduce. */
 occlResult_t occlCollBlocks(occlComm_t comm, int kind, size_t count, occlDataType_t datatype,
                             int* nblocks);
 

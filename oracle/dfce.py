@@ -245,7 +245,7 @@ def lane_geometry(meta: CollMeta, n: int, rank: int, cfg: SimConfig):
     elif meta.kind == "allgather":
         segs = [(0 if q == rank else None, q * N, N) for q in range(n)]
         seglen = N
-    elif meta.kind == "broadcast":
+    elif meta.kind in ("broadcast", "reduce"):
         segs = [(0, 0, N)]
         seglen = N
     else:

@@ -15,6 +15,8 @@ its textbook definition; in floating point the reduction ORDER is the ring's:
   RS  out_r[j]      = the same fold with c = r over x_q[r*N + j]
   AG  out[q*N + j]  = x_q[j]
   BC  out           = x_root
+  RED out_root      = ((x_{root+1} (+) x_{root+2}) (+) ...) (+) x_root   (recv buffers of the
+                      other ranks are not written; NCCL's ring Reduce chain)
   n = 1             => copy
 
 Indices are mod n.  (+) is the collective's reducing function (PAPER.md:306
@@ -38,6 +40,7 @@ import numpy as np
 from inputs import hashgen
 
 KINDS = ("allreduce", "allgather", "reducescatter", "broadcast")
+ALL_KINDS = KINDS + ("reduce",)
 ITEMSIZE = {"i32": 4, "f32": 4, "bf16": 2, "f16": 2}
 OPS = ("sum", "prod", "max", "min")
 
@@ -157,6 +160,14 @@ def broadcast(xs, root: int) -> np.ndarray:
     return np.array(xs[root], copy=True)
 
 
+def reduce(xs, dtype: str, root: int, op: str = "sum") -> np.ndarray:
+    """Reduce to root: the chain root+1 -> root+2 -> ... -> root, folded in that order."""
+    n = len(xs)
+    if n == 1:
+        return np.array(xs[0], copy=True)
+    return ring_fold([xs[q] for q in fold_order(root, n)], dtype, op)
+
+
 # ----------------------------------------------------------------------------- sampled results
 def expected_at(kind: str, dtype: str, n: int, count: int, seed: int, coll: int,
                 idx, rank: int = 0, root: int = 0, op: str = "sum") -> np.ndarray:
@@ -174,7 +185,9 @@ def expected_at(kind: str, dtype: str, n: int, count: int, seed: int, coll: int,
             m = q == src
             out[m] = val(src, idx[m] - src * count)
         return out
-    if kind == "broadcast" or n == 1:
+    if kind == "reduce" and n > 1:
+        return ring_fold([val(q, idx) for q in fold_order(root, n)], dtype, op)
+    if kind in ("broadcast", "reduce") or n == 1:
         if kind == "reducescatter":
             return val(0, idx)
         return val(root if kind == "broadcast" else 0, idx)
@@ -212,6 +225,8 @@ def result_full(kind: str, dtype: str, xs, root: int = 0, op: str = "sum"):
     if kind == "broadcast":
         o = broadcast(xs, root)
         return [o] * n
+    if kind == "reduce":
+        return [reduce(xs, dtype, root, op) if r == root else None for r in range(n)]   # root only
     raise ValueError(kind)
 
 
@@ -264,4 +279,12 @@ def ring_sequence(kind: str, n: int, r: int, root: int = 0, inplace: bool = Fals
         if pos == n - 1:
             return [("Recv", 0)]
         return [("RecvCopySend", 0)]
+    if kind == "reduce":
+        # chain root+1 -> ... -> root (NCCL ring Reduce); one segment
+        pos = m(r - root - 1)
+        if pos == 0:
+            return [("Send", 0)]
+        if pos == n - 1:
+            return [("RecvReduceCopy", 0)]
+        return [("RecvReduceSend", 0)]
     raise ValueError(kind)

@@ -288,6 +288,14 @@ __device__ __forceinline__ void step_prim(int kind, int n, int r, int root, int 
       else if (step < n - 1) { prim = P_RECVCOPYSEND; seg = md(r - step, n); }
       else { prim = P_RECV; seg = md(r + 1, n); }
       return;
+    case kReduce: {  // chain root+1 -> root+2 -> ... -> root (NCCL ring Reduce), one segment
+      const int pos = md(r - root - 1, n);
+      seg = 0;
+      if (pos == 0) prim = P_SEND;
+      else if (pos == n - 1) prim = P_RECVREDUCECOPY;
+      else prim = P_RECVREDUCESEND;
+      return;
+    }
     default: {  // broadcast: chain root -> root+1 -> ... -> root-1
       const int pos = md(r - root, n);
       seg = 0;
@@ -307,7 +315,7 @@ __device__ __forceinline__ void step_prim(int kind, int n, int r, int root, int 
 // head / credit protocol is unchanged (a direct message still takes a connector
 // sequence number), so flow control and resume are exactly as before.
 __device__ __forceinline__ int directify(int prim, int kind, int n, int step, bool dOut, bool dIn) {
-  if (n == 1 || kind == kReduceScatter) return prim;
+  if (n == 1 || kind == kReduceScatter || kind == kReduce) return prim;   // partial sums are not final
   const bool agPhase = kind != kAllReduce || step >= n - 1;    // data on the wire is final
   if (dOut && agPhase && (prim & A_SEND)) prim |= A_DOUT;
   const bool finalIn = kind != kAllReduce || step >= n;          // received data is final
@@ -320,7 +328,7 @@ __device__ __forceinline__ int elem_size(int dt) { return (dt == kBF16 || dt == 
 // Segment q's base offsets (elements) in the send / recv buffers and length.
 __device__ __forceinline__ void seg_geom(int kind, int n, int r, uint64_t count, uint64_t segLen, int q,
                                          uint64_t& sendOff, uint64_t& recvOff, uint64_t& len) {
-  if (n == 1 || kind == kBroadcast) { sendOff = 0; recvOff = 0; len = count; return; }
+  if (n == 1 || kind == kBroadcast || kind == kReduce) { sendOff = 0; recvOff = 0; len = count; return; }
   switch (kind) {
     case kAllReduce: {
       const uint64_t lo = (uint64_t)q * segLen;
@@ -457,7 +465,7 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched
   uint64_t nloops = (part + chunk - 1) / chunk;
   if (nloops == 0) nloops = 1;
   int nsteps = 1;
-  if (n > 1) nsteps = e.kind == kAllReduce ? 2 * n - 1 : (e.kind == kBroadcast ? 1 : n);
+  if (n > 1) nsteps = e.kind == kAllReduce ? 2 * n - 1 : ((e.kind == kBroadcast || e.kind == kReduce) ? 1 : n);
   const uint64_t nsent = g->d.nsent, nrecv = g->d.nrecv;
   uint4 w[kCtxBytes / 16];
   CtxSlot* ns = reinterpret_cast<CtxSlot*>(w);

@@ -398,7 +398,7 @@ occlResult_t submit(occlComm* sc, int kind, int dtype, int op, int root, size_t 
   if (collId >= c->cfg.maxColl) return occlRegistryFull;
   if (dtype < 0 || dtype > 3) return occlInvalidArgument;
   if (op < occlSum || op > occlMin) return occlInvalidArgument;
-  if (kind == kBroadcast && (root < 0 || root >= sc->nranks)) return occlInvalidArgument;
+  if ((kind == kBroadcast || kind == kReduce) && (root < 0 || root >= sc->nranks)) return occlInvalidArgument;
   if (count > 0 && (!send || !recv)) return occlInvalidArgument;
   if (c->state[collId].load() == 1 && !try_complete(c, collId)) return occlDuplicateSubmit;
   c->subSeq[collId]++;
@@ -928,6 +928,10 @@ occlResult_t occlReduceScatter(const void* s, void* r, size_t recvcount, occlDat
 occlResult_t occlBroadcast(const void* s, void* r, size_t count, occlDataType_t dt, int root, int id, occlComm_t c) {
   return submit(c, kBroadcast, dt, occlSum, root, count, s, r, id);
 }
+occlResult_t occlReduce(const void* s, void* r, size_t count, occlDataType_t dt, occlRedOp_t op, int root, int id,
+                        occlComm_t c) {
+  return submit(c, kReduce, dt, op, root, count, s, r, id);
+}
 
 occlResult_t occlTest(occlComm_t c, int id, int* done) {
   c = root_of(c);                                      // sub-communicators use their root's daemon
@@ -1151,7 +1155,7 @@ occlResult_t occlCommGetStream(occlComm_t c, void** stream) {
 }
 
 occlResult_t occlCollBlocks(occlComm_t c, int kind, size_t count, occlDataType_t dt, int* nblocks) {
-  if (!c || !nblocks || kind < 0 || kind > 3 || dt < 0 || dt > 3) return occlInvalidArgument;
+  if (!c || !nblocks || kind < 0 || kind > 4 || dt < 0 || dt > 3) return occlInvalidArgument;
   *nblocks = coll_blocks(c, kind, count, dt);
   return occlSuccess;
 }

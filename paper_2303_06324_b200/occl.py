@@ -26,7 +26,7 @@ occlInt32, occlFloat32, occlBfloat16, occlFloat16 = 0, 1, 2, 3
 occlSum, occlProd, occlMax, occlMin = 0, 1, 2, 3
 OPS = {"sum": occlSum, "prod": occlProd, "max": occlMax, "min": occlMin}
 occlOrderFifo, occlOrderPriority = 0, 1
-KIND = {"allreduce": 0, "allgather": 1, "reducescatter": 2, "broadcast": 3}
+KIND = {"allreduce": 0, "allgather": 1, "reducescatter": 2, "broadcast": 3, "reduce": 4}
 DTYPE = {"i32": occlInt32, "f32": occlFloat32, "bf16": occlBfloat16, "f16": occlFloat16}
 OCCL_HANDLE_BYTES = 256
 
@@ -36,7 +36,7 @@ EXPORTED = [
     "occlBroadcast", "occlWait", "occlTest", "occlSetCallback", "occlGetStats", "occlGetCollStats",
     "occlCommExit", "occlCommLaunch", "occlCommSetAutoLaunch", "occlCommQuiesce", "occlCommGetStream",
     "occlCollBlocks", "occlCommFuse", "occlGetProbes", "occlSetPriority", "occlGetTrace", "occlTraceReset",
-    "occlCommSplit",
+    "occlCommSplit", "occlReduce",
 ]
 TRACE_EVENTS = {1: "fetch", 2: "switch_in", 3: "issue", 4: "publish", 5: "preempt", 6: "done", 7: "cqe",
                 8: "quit", 9: "exit", 10: "sdone", 11: "start", 12: "mark"}
@@ -110,6 +110,7 @@ def _lib():
             "occlAllGather": [vp, vp, sz, i, i, vp],
             "occlReduceScatter": [vp, vp, sz, i, i, i, vp],
             "occlBroadcast": [vp, vp, sz, i, i, i, vp],
+            "occlReduce": [vp, vp, sz, i, i, i, i, vp],
             "occlWait": [vp, i, i64],
             "occlTest": [vp, i, C.POINTER(i)],
             "occlSetCallback": [vp, i, CALLBACK, vp],
@@ -273,6 +274,12 @@ class Comm:
         dtype = _dt(recv) if dtype is None else dtype
         check(occlBroadcast(_ptr(send), _ptr(recv), count, dtype, root, coll_id, self.h), "occlBroadcast")
 
+    def reduce(self, send, recv, root, coll_id, count=None, dtype=None, op="sum"):
+        count = send.numel() if count is None else count
+        dtype = _dt(send) if dtype is None else dtype
+        check(_lib().occlReduce(_ptr(send), _ptr(recv), count, dtype, OPS.get(op, op), root, coll_id, self.h),
+              "occlReduce")
+
     def submit(self, kind, send, recv, coll_id, count, dtype, root=0, op="sum"):
         k = KIND[kind] if isinstance(kind, str) else kind
         d = DTYPE[dtype] if isinstance(dtype, str) else dtype
@@ -283,8 +290,10 @@ class Comm:
             r = occlAllGather(_ptr(send), _ptr(recv), count, d, coll_id, self.h)
         elif k == 2:
             r = occlReduceScatter(_ptr(send), _ptr(recv), count, d, o, coll_id, self.h)
-        else:
+        elif k == 3:
             r = occlBroadcast(_ptr(send), _ptr(recv), count, d, root, coll_id, self.h)
+        else:
+            r = _lib().occlReduce(_ptr(send), _ptr(recv), count, d, o, root, coll_id, self.h)
         check(r, f"submit {kind}")
 
     # completion ------------------------------------------------------------------

@@ -83,3 +83,28 @@ def test_f16_copies(rings, kind):
         sends, recvs = U.make_bufs(kind, "f16", 8, count, 77, 30)
         U.run_collective(comms, kind, sends, recvs, 30, count, "f16", root=5)
         U.check_full(kind, "f16", 8, count, 77, 30, recvs, root=5)
+
+
+@pytest.mark.parametrize("op", OPS)
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("n", [1, 2, 3, 8])
+def test_reduce_to_root(rings, op, dtype, n):
+    """Reduce (NCCL ring chain root+1 -> ... -> root): the root's output is the
+    oracle's fold in chain order, bit-exact; other ranks' recv buffers untouched."""
+    from oracle import ring
+    for big in (False, True):
+        if big and n != 8:
+            continue
+        comms = rings(n, big)
+        for ci, count in enumerate([1, 5_003, 300_001] if big else [1, 5_003]):
+            root = (ci + 1) % n
+            cid = 40 + ci
+            seed = 3000 + ci + 10 * OPS.index(op)
+            sends, recvs = U.make_bufs("allreduce", dtype, n, count, seed, cid)   # same buffer shapes
+            before = [U.to_np_bits(r) for r in recvs]
+            U.run_collective(comms, "reduce", sends, recvs, cid, count, dtype, root=root, op=op)
+            xs = ring.inputs_full("allreduce", dtype, n, count, seed, cid)
+            exp = U.bits(ring.reduce(xs, dtype, root, op))
+            for r in range(n):
+                got = U.to_np_bits(recvs[r])
+                assert np.array_equal(got, exp if r == root else before[r]), (r, root, count)
