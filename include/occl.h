@@ -66,11 +66,12 @@ typedef enum {
   occlInternalError = 11     /* corrupt context or invariant violation                         */
 } occlResult_t;
 
-typedef enum { occlInt32 = 0, occlFloat32 = 1, occlBfloat16 = 2, occlFloat16 = 3 } occlDataType_t;
+typedef enum { occlInt32 = 0, occlFloat32 = 1, occlBfloat16 = 2, occlFloat16 = 3, occlInt64 = 4,
+               occlFloat64 = 5 } occlDataType_t;
 /* The collective's reducing function ("a specified reducing
  * function").  Results are bit-exact with the ring's fold order: IEEE
- * round-to-nearest-even per hop for f32 / bf16 / f16, two's-complement wrap for
- * i32 sum and prod, exact max / min. */
+ * round-to-nearest-even per hop for f64 / f32 / bf16 / f16, two's-complement wrap
+ * for integer sum and prod, exact max / min. */
 typedef enum { occlSum = 0, occlProd = 1, occlMax = 2, occlMin = 3 } occlRedOp_t;
 typedef enum { occlOrderFifo = 0, occlOrderPriority = 1 } occlOrderPolicy_t;
 

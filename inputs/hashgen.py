@@ -20,6 +20,9 @@ so no rounding happens during generation and the GPU generator in
             x = (m - 1024) * 2^(-10 - e)          exact in IEEE binary16 (11 sig. bits,
             2^-17 >= the smallest normal's ulp range); stored as numpy float16.
 * ``i32`` : low 32 bits of u, as two's-complement int32.
+* ``i64`` : all 64 bits of u, as two's-complement int64.
+* ``f64`` : m = u >> 11 (53 bits), e = (u >> 32) & 7,
+            x = (m - 2^52) * 2^(-52 - e)          exact in binary64.
 
 This module holds no arithmetic of the collective method.
 """
@@ -29,9 +32,10 @@ import numpy as np
 
 MASK64 = (1 << 64) - 1
 
-DTYPES = ("i32", "f32", "bf16", "f16")
-ITEMSIZE = {"i32": 4, "f32": 4, "bf16": 2, "f16": 2}
-NP_STORAGE = {"i32": np.int32, "f32": np.float32, "bf16": np.uint16, "f16": np.float16}
+DTYPES = ("i32", "f32", "bf16", "f16", "i64", "f64")
+ITEMSIZE = {"i32": 4, "f32": 4, "bf16": 2, "f16": 2, "i64": 8, "f64": 8}
+NP_STORAGE = {"i32": np.int32, "f32": np.float32, "bf16": np.uint16, "f16": np.float16, "i64": np.int64,
+              "f64": np.float64}
 
 
 def splitmix64(x: np.ndarray) -> np.ndarray:
@@ -54,6 +58,8 @@ def values(dtype: str, seed: int, coll: int, rank: int, idx) -> np.ndarray:
         u = splitmix64(keys(seed, coll, rank, np.asarray(idx, dtype=np.uint64)))
     if dtype == "i32":
         return (u & np.uint64(0xFFFFFFFF)).astype(np.uint32).view(np.int32)
+    if dtype == "i64":
+        return u.view(np.int64)
     e = ((u >> np.uint64(32)) & np.uint64(7)).astype(np.int64)
     if dtype == "f32":
         m = (u >> np.uint64(40)).astype(np.int64) - (1 << 23)
@@ -65,6 +71,9 @@ def values(dtype: str, seed: int, coll: int, rank: int, idx) -> np.ndarray:
     if dtype == "f16":
         m = (u >> np.uint64(53)).astype(np.int64) - 1024
         return np.ldexp(m.astype(np.float64), -10 - e).astype(np.float16)
+    if dtype == "f64":
+        m = (u >> np.uint64(11)).astype(np.int64) - (1 << 52)
+        return np.ldexp(m.astype(np.float64), -52 - e)
     raise ValueError(f"unknown dtype {dtype!r}")
 
 

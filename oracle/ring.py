@@ -28,6 +28,8 @@ Indices are mod n.  (+) is the collective's reducing function (PAPER.md:306
          a bf16 product is exact in f32, and for sums double rounding is innocuous
          since 24 >= 2*8 + 2)
   f16  : RNE_f16(float32(a) op float32(b))   (same argument, 24 >= 2*11 + 2)
+  i64  : two's-complement wrap (sum, prod), signed max / min
+  f64  : IEEE-754 binary64, round-to-nearest-even (numpy float64)
   max / min are exact (no rounding); inputs carry no NaN.
 
 Where the paper is silent (segment map, operand order, bf16 partial precision)
@@ -41,7 +43,7 @@ from inputs import hashgen
 
 KINDS = ("allreduce", "allgather", "reducescatter", "broadcast")
 ALL_KINDS = KINDS + ("reduce",)
-ITEMSIZE = {"i32": 4, "f32": 4, "bf16": 2, "f16": 2}
+ITEMSIZE = {"i32": 4, "f32": 4, "bf16": 2, "f16": 2, "i64": 8, "f64": 8}
 OPS = ("sum", "prod", "max", "min")
 
 
@@ -92,6 +94,21 @@ def add(a: np.ndarray, b: np.ndarray, dtype: str, op: str = "sum") -> np.ndarray
     if dtype == "f16":
         return _f32_op(np.asarray(a, dtype=np.float16).astype(np.float32),
                        np.asarray(b, dtype=np.float16).astype(np.float32), op).astype(np.float16)
+    if dtype == "i64":
+        ua, ub = np.asarray(a).view(np.uint64), np.asarray(b).view(np.uint64)
+        if op == "sum":
+            return (ua + ub).view(np.int64)            # mod 2^64
+        if op == "prod":
+            return (ua * ub).view(np.int64)
+        ia, ib = np.asarray(a).view(np.int64), np.asarray(b).view(np.int64)
+        return np.maximum(ia, ib) if op == "max" else np.minimum(ia, ib)
+    if dtype == "f64":
+        x, y = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+        if op == "sum":
+            return x + y
+        if op == "prod":
+            return x * y
+        return np.maximum(x, y) if op == "max" else np.minimum(x, y)
     raise ValueError(dtype)
 
 

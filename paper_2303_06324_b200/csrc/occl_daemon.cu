@@ -142,6 +142,25 @@ template <int OP> __device__ __forceinline__ uint32_t op_f16x2(uint32_t a, uint3
   else z = __hmin2(x, y);
   return *reinterpret_cast<uint32_t*>(&z);
 }
+template <int OP> __device__ __forceinline__ uint64_t op_i64(uint64_t a, uint64_t b) {
+  if constexpr (OP == kSum) return a + b;
+  else if constexpr (OP == kProd) return a * b;
+  else if constexpr (OP == kMax) return (uint64_t)max((long long)a, (long long)b);
+  else return (uint64_t)min((long long)a, (long long)b);
+}
+template <int OP> __device__ __forceinline__ uint64_t op_f64(uint64_t a, uint64_t b) {
+  const double x = __longlong_as_double((long long)a), y = __longlong_as_double((long long)b);
+  double z;
+  if constexpr (OP == kSum) z = __dadd_rn(x, y);
+  else if constexpr (OP == kProd) z = __dmul_rn(x, y);
+  else if constexpr (OP == kMax) z = fmax(x, y);
+  else z = fmin(x, y);
+  return (uint64_t)__double_as_longlong(z);
+}
+template <int DT, int OP> __device__ __forceinline__ uint64_t op_d(uint64_t a, uint64_t b) {
+  if constexpr (DT == kI64) return op_i64<OP>(a, b);
+  else return op_f64<OP>(a, b);
+}
 // one 32-bit lane of packed elements
 template <int DT, int OP> __device__ __forceinline__ uint32_t op_w(uint32_t a, uint32_t b) {
   if constexpr (DT == kF32) return op_f32<OP>(a, b);
@@ -150,7 +169,14 @@ template <int DT, int OP> __device__ __forceinline__ uint32_t op_w(uint32_t a, u
   else return op_f16x2<OP>(a, b);
 }
 template <int DT, int OP> __device__ __forceinline__ uint4 vop(const uint4& a, const uint4& b) {
-  return make_uint4(op_w<DT, OP>(a.x, b.x), op_w<DT, OP>(a.y, b.y), op_w<DT, OP>(a.z, b.z), op_w<DT, OP>(a.w, b.w));
+  if constexpr (DT == kI64 || DT == kF64) {           // two 64-bit elements per vector
+    const uint64_t lo = op_d<DT, OP>(((uint64_t)a.y << 32) | a.x, ((uint64_t)b.y << 32) | b.x);
+    const uint64_t hi = op_d<DT, OP>(((uint64_t)a.w << 32) | a.z, ((uint64_t)b.w << 32) | b.z);
+    return make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
+  } else {
+    return make_uint4(op_w<DT, OP>(a.x, b.x), op_w<DT, OP>(a.y, b.y), op_w<DT, OP>(a.z, b.z),
+                      op_w<DT, OP>(a.w, b.w));
+  }
 }
 
 // ------------------------------------------------------------------ primitives
@@ -189,11 +215,15 @@ template <> struct Elem<kF32> { typedef uint32_t T; };
 template <> struct Elem<kI32> { typedef uint32_t T; };
 template <> struct Elem<kBF16> { typedef uint16_t T; };
 template <> struct Elem<kF16> { typedef uint16_t T; };
+template <> struct Elem<kI64> { typedef uint64_t T; };
+template <> struct Elem<kF64> { typedef uint64_t T; };
 
 // one element (bit pattern) of the reducing function
 template <int DT, int OP>
 __device__ __forceinline__ typename Elem<DT>::T sop(typename Elem<DT>::T a, typename Elem<DT>::T b) {
-  if constexpr (sizeof(typename Elem<DT>::T) == 4) {
+  if constexpr (sizeof(typename Elem<DT>::T) == 8) {
+    return op_d<DT, OP>(a, b);
+  } else if constexpr (sizeof(typename Elem<DT>::T) == 4) {
     return op_w<DT, OP>(a, b);
   } else {
     return (typename Elem<DT>::T)(op_w<DT, OP>((uint32_t)a, (uint32_t)b) & 0xffffu);   // low half only
@@ -323,7 +353,9 @@ __device__ __forceinline__ int directify(int prim, int kind, int n, int step, bo
   return prim;
 }
 
-__device__ __forceinline__ int elem_size(int dt) { return (dt == kBF16 || dt == kF16) ? 2 : 4; }
+__device__ __forceinline__ int elem_size(int dt) {
+  return (dt == kBF16 || dt == kF16) ? 2 : ((dt == kI64 || dt == kF64) ? 8 : 4);
+}
 
 // Segment q's base offsets (elements) in the send / recv buffers and length.
 __device__ __forceinline__ void seg_geom(int kind, int n, int r, uint64_t count, uint64_t segLen, int q,
@@ -1057,7 +1089,7 @@ __device__ __forceinline__ uint4 lds_v4(const void* p) {
 // compute warps move it with register loads (move_slice).
 __device__ __forceinline__ int tma_vec_bytes(int dtype, int64_t nelem, const char* src, const char* dst,
                                              const char* cout) {
-  const int isz = (dtype == kBF16 || dtype == kF16) ? 2 : 4;
+  const int isz = elem_size(dtype);
   if (nelem <= 0) return 0;
   if ((((uintptr_t)src) | ((uintptr_t)dst) | ((uintptr_t)cout)) & 15) return 0;   // cout: a peer buffer (direct)
   const int vb = (int)((nelem * isz) & ~(int64_t)15);
@@ -1224,7 +1256,15 @@ __device__ __forceinline__ void tail_slice(const int prim, const char* src, cons
       case kF16 * 4 + kSum: FN<kF16, kSum>(__VA_ARGS__); break;                    \
       case kF16 * 4 + kProd: FN<kF16, kProd>(__VA_ARGS__); break;                  \
       case kF16 * 4 + kMax: FN<kF16, kMax>(__VA_ARGS__); break;                    \
-      default: FN<kF16, kMin>(__VA_ARGS__); break;                                 \
+      case kF16 * 4 + kMin: FN<kF16, kMin>(__VA_ARGS__); break;                    \
+      case kI64 * 4 + kSum: FN<kI64, kSum>(__VA_ARGS__); break;                    \
+      case kI64 * 4 + kProd: FN<kI64, kProd>(__VA_ARGS__); break;                  \
+      case kI64 * 4 + kMax: FN<kI64, kMax>(__VA_ARGS__); break;                    \
+      case kI64 * 4 + kMin: FN<kI64, kMin>(__VA_ARGS__); break;                    \
+      case kF64 * 4 + kSum: FN<kF64, kSum>(__VA_ARGS__); break;                    \
+      case kF64 * 4 + kProd: FN<kF64, kProd>(__VA_ARGS__); break;                  \
+      case kF64 * 4 + kMax: FN<kF64, kMax>(__VA_ARGS__); break;                    \
+      default: FN<kF64, kMin>(__VA_ARGS__); break;                                 \
     }                                                                              \
   } while (0)
 

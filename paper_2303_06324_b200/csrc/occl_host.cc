@@ -58,7 +58,7 @@ inline void cpu_relax() {
 #endif
 }
 
-int elem_size(int dt) { return (dt == kBF16 || dt == kF16) ? 2 : 4; }
+int elem_size(int dt) { return (dt == kBF16 || dt == kF16) ? 2 : ((dt == kI64 || dt == kF64) ? 8 : 4); }
 
 uint64_t fingerprint(const occlConfig_t& c) {
   uint64_t h = 1469598103934665603ull;
@@ -396,7 +396,7 @@ occlResult_t submit(occlComm* sc, int kind, int dtype, int op, int root, size_t 
   if (comm_sticky(c)) return occlCudaError;
   if (collId < 0) return occlInvalidArgument;
   if (collId >= c->cfg.maxColl) return occlRegistryFull;
-  if (dtype < 0 || dtype > 3) return occlInvalidArgument;
+  if (dtype < 0 || dtype > 5) return occlInvalidArgument;
   if (op < occlSum || op > occlMin) return occlInvalidArgument;
   if ((kind == kBroadcast || kind == kReduce) && (root < 0 || root >= sc->nranks)) return occlInvalidArgument;
   if (count > 0 && (!send || !recv)) return occlInvalidArgument;
@@ -1155,7 +1155,7 @@ occlResult_t occlCommGetStream(occlComm_t c, void** stream) {
 }
 
 occlResult_t occlCollBlocks(occlComm_t c, int kind, size_t count, occlDataType_t dt, int* nblocks) {
-  if (!c || !nblocks || kind < 0 || kind > 4 || dt < 0 || dt > 3) return occlInvalidArgument;
+  if (!c || !nblocks || kind < 0 || kind > 4 || dt < 0 || dt > 5) return occlInvalidArgument;
   *nblocks = coll_blocks(c, kind, count, dt);
   return occlSuccess;
 }

@@ -7,7 +7,7 @@
 namespace occl {
 
 enum Kind : uint16_t { kAllReduce = 0, kAllGather = 1, kReduceScatter = 2, kBroadcast = 3, kReduce = 4, kExit = 15 };
-enum Dtype : uint16_t { kI32 = 0, kF32 = 1, kBF16 = 2, kF16 = 3 };
+enum Dtype : uint16_t { kI32 = 0, kF32 = 1, kBF16 = 2, kF16 = 3, kI64 = 4, kF64 = 5 };
 
 constexpr int kMaxRanks = 64;
 constexpr int kFlagStride = 384;        // per (coll, block): head @+0, credit @+128, direct @+256 (own lines)

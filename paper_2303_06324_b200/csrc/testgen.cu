@@ -8,6 +8,8 @@
 //   bf16: (int(u >> 56) - 128)  * 2^(-7  - ((u >> 32) & 7))   (exact, top 16 bits)
 //   f16 : (int(u >> 53) - 1024) * 2^(-10 - ((u >> 32) & 7))  (exact in binary16)
 //   i32 : low 32 bits of u
+//   i64 : all 64 bits of u
+//   f64 : (int(u >> 11) - 2^52) * 2^(-52 - ((u >> 32) & 7))   (exact in binary64)
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include <stdint.h>
@@ -34,9 +36,14 @@ __global__ void fill_kernel(void* dst, uint64_t count, int dtype, uint64_t base,
       const int m = (int)(u >> 56) - 128;
       const float f = ldexpf((float)m, -7 - e);
       reinterpret_cast<uint16_t*>(dst)[i] = (uint16_t)(__float_as_uint(f) >> 16);
-    } else {
+    } else if (dtype == 3) {
       const int m = (int)(u >> 53) - 1024;
       reinterpret_cast<__half*>(dst)[i] = __float2half_rn(ldexpf((float)m, -10 - e));   // exact
+    } else if (dtype == 4) {
+      reinterpret_cast<uint64_t*>(dst)[i] = u;
+    } else {
+      const long long m = (long long)(u >> 11) - (1ll << 52);
+      reinterpret_cast<double*>(dst)[i] = ldexp((double)m, -52 - e);                      // exact
     }
   }
 }

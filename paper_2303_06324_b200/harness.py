@@ -15,8 +15,9 @@ import torch
 
 from . import occl
 
-TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32, "f16": torch.float16}
-ITEM = {"f32": 4, "bf16": 2, "i32": 4, "f16": 2}
+TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32, "f16": torch.float16,
+            "i64": torch.int64, "f64": torch.float64}
+ITEM = {"f32": 4, "bf16": 2, "i32": 4, "f16": 2, "i64": 8, "f64": 8}
 
 
 def ring(nranks, device=0, dist=None, world=1, prank=0, **cfg):

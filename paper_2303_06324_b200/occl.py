@@ -22,12 +22,13 @@ GEN_PATH = os.path.join(_HERE, "lib", "libocclgen.so")
 occlSuccess, occlInvalidArgument, occlInvalidUsage, occlRegistryFull, occlQueueFull, \
     occlDuplicateSubmit, occlUnknownId, occlCudaError, occlSystemError, occlTimeout, \
     occlInProgress, occlInternalError = range(12)
-occlInt32, occlFloat32, occlBfloat16, occlFloat16 = 0, 1, 2, 3
+occlInt32, occlFloat32, occlBfloat16, occlFloat16, occlInt64, occlFloat64 = 0, 1, 2, 3, 4, 5
 occlSum, occlProd, occlMax, occlMin = 0, 1, 2, 3
 OPS = {"sum": occlSum, "prod": occlProd, "max": occlMax, "min": occlMin}
 occlOrderFifo, occlOrderPriority = 0, 1
 KIND = {"allreduce": 0, "allgather": 1, "reducescatter": 2, "broadcast": 3, "reduce": 4}
-DTYPE = {"i32": occlInt32, "f32": occlFloat32, "bf16": occlBfloat16, "f16": occlFloat16}
+DTYPE = {"i32": occlInt32, "f32": occlFloat32, "bf16": occlBfloat16, "f16": occlFloat16, "i64": occlInt64,
+         "f64": occlFloat64}
 OCCL_HANDLE_BYTES = 256
 
 EXPORTED = [
@@ -380,7 +381,7 @@ class Comm:
 def _dt(t):
     import torch
     return {torch.float32: occlFloat32, torch.bfloat16: occlBfloat16, torch.int32: occlInt32,
-            torch.float16: occlFloat16}[t.dtype]
+            torch.float16: occlFloat16, torch.int64: occlInt64, torch.float64: occlFloat64}[t.dtype]
 
 
 def occlCommFuse(comms):

@@ -9,21 +9,22 @@ from inputs import hashgen
 from oracle import ring
 from paper_2303_06324_b200 import occl
 
-TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32, "f16": torch.float16}
+TORCH_DT = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32, "f16": torch.float16,
+            "i64": torch.int64, "f64": torch.float64}
 WAIT_S = 60.0
 
 
 def bits(a):
     a = np.asarray(a)
-    return a.view(np.uint32) if a.dtype.itemsize == 4 else a.view(np.uint16)
+    return a.view({8: np.uint64, 4: np.uint32, 2: np.uint16}[a.dtype.itemsize])
 
 
 def to_np_bits(t: torch.Tensor) -> np.ndarray:
     t = t.detach().cpu()
     if t.dtype in (torch.bfloat16, torch.float16):
         return t.view(torch.int16).numpy().view(np.uint16)
-    if t.dtype == torch.float32:
-        return t.numpy().view(np.uint32)
+    if t.dtype in (torch.int64, torch.float64):
+        return t.numpy().view(np.uint64)
     return t.numpy().view(np.uint32)
 
 

@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 import gpu_util as U  # noqa: E402
 
 OPS = ["sum", "prod", "max", "min"]
-DTYPES = ["f32", "bf16", "f16", "i32"]
+DTYPES = ["f32", "bf16", "f16", "i32", "i64", "f64"]
 
 
 @pytest.fixture(scope="module")
@@ -41,12 +41,12 @@ def rings(occl_mod):
         occl_mod.destroy_group(comms)
 
 
-def test_f16_generator_matches_numpy(occl_mod):
-    t = torch.empty(70_001, dtype=torch.float16, device=0)
-    occl_mod.test_fill(t, "f16", 0x55, 3, 2, offset=9)
+@pytest.mark.parametrize("dtype", ["f16", "i64", "f64"])
+def test_new_dtype_generators_match_numpy(occl_mod, dtype):
+    t = torch.empty(70_001, dtype=U.TORCH_DT[dtype], device=0)
+    occl_mod.test_fill(t, dtype, 0x55, 3, 2, offset=9)
     torch.cuda.synchronize()
-    exp = hashgen.values("f16", 0x55, 3, 2, np.arange(9, 9 + 70_001)).view(np.uint16)
-    assert np.array_equal(U.to_np_bits(t), exp)
+    assert np.array_equal(U.to_np_bits(t), U.bits(hashgen.values(dtype, 0x55, 3, 2, np.arange(9, 9 + 70_001))))
 
 
 @pytest.mark.parametrize("op", OPS)

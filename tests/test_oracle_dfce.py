@@ -22,7 +22,7 @@ GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_
 
 def _bits(a):
     a = np.asarray(a)
-    return a.view(np.uint32) if a.dtype.itemsize == 4 else a.view(np.uint16)
+    return a.view({8: np.uint64, 4: np.uint32, 2: np.uint16}[a.dtype.itemsize])
 
 
 def _check_results(sim, bufs, metas, n, iterations=1):

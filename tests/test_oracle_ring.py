@@ -21,7 +21,7 @@ COUNTS = [1, 7, 256, 1000, 65536]
 
 def _bits(a):
     a = np.asarray(a)
-    return a.view(np.uint32) if a.dtype.itemsize == 4 else a.view(np.uint16)
+    return a.view({8: np.uint64, 4: np.uint32, 2: np.uint16}[a.dtype.itemsize])
 
 
 # ------------------------------------------------------------------ SPEC / paper examples
@@ -424,3 +424,40 @@ def test_reduce_in_random_orders_completes():
         sim, bufs = dfce.run_orders(metas, [list(o) for o in orders], cfg, seed=si)
         xs = [bufs[(r, 1, 0)][0] for r in range(2)]
         assert np.array_equal(_bits(sim.results[(1, 1, 0)]), _bits(ring.reduce(xs, "f32", 1)))
+
+
+# ------------------------------------------------------------------ 64-bit types
+def test_64bit_generators_exact_and_ops():
+    """i64 wraps mod 2^64 (closed form on rank-constant inputs), f64 inputs are
+    exact (m - 2^52) * 2^(-52-e) and fold in the ring order like f32."""
+    n = 4
+    xs = [np.full(300, (1 << 62) + r, dtype=np.int64) for r in range(n)]
+    s = ring.allreduce(xs, "i64")
+    assert np.all(s == np.int64(((4 << 62) + 6) % (1 << 64)))              # 2^64 wraps to 0, + 0+1+2+3
+    assert np.all(ring.allreduce(xs, "i64", "max") == (1 << 62) + 3)
+    v = hashgen.values("f64", 9, 1, 2, np.arange(4000))
+    for x in v[:500].tolist():
+        f = Fraction(x)
+        assert any((f * 2 ** (52 + e)).denominator == 1 for e in range(8))
+    xs = ring.inputs_full("allreduce", "f64", 8, 4096, 3, 3)
+    o = ring.allreduce(xs, "f64")
+    naive = xs[0].copy()
+    for x in xs[1:]:
+        naive = naive + x
+    assert (o.view(np.uint64) != naive.view(np.uint64)).any()               # order observable
+    assert np.allclose(o, naive, rtol=1e-12, atol=1e-18)
+
+
+@pytest.mark.parametrize("op", ["sum", "prod", "max", "min"])
+@pytest.mark.parametrize("dtype", ["i64", "f64"])
+def test_o1_equals_o2_execution_64bit(op, dtype):
+    n = 3
+    for kind in ("allreduce", "reducescatter", "reduce"):
+        meta = dfce.CollMeta(0, kind, dtype, 37, nblocks=2, op=op, root=1)
+        cfg = dfce.SimConfig(lanes=2, K=3, slice_elems=4, slices_per_chunk=2, seed=1)
+        sim, bufs = dfce.run_orders([meta], [[0]] * n, cfg, seed=7)
+        xs = [bufs[(r, 0, 0)][0] for r in range(n)]
+        exp = ring.result_full(kind, dtype, xs, root=1, op=op)
+        for r in range(n):
+            if exp[r] is not None:
+                assert np.array_equal(_bits(sim.results[(r, 0, 0)]), _bits(exp[r])), (kind, r)
