@@ -165,6 +165,19 @@ typedef struct {
 enum { occlEvFetch = 1, occlEvSwitchIn = 2, occlEvIssue = 3, occlEvPublish = 4, occlEvPreempt = 5,
        occlEvDone = 6, occlEvCqe = 7, occlEvQuit = 8, occlEvExit = 9, occlEvSdone = 10, occlEvStart = 11, occlEvMark = 12 };
 
+/* Memory footprint of one rank (PAPER.md:581-582 reports "about 4 MB of global
+ * memory per block for 1,000 collectives"; reading Q15 of SURVEY.md).  Bytes. */
+typedef struct {
+  uint64_t device;          /* total device memory of the communicator           */
+  uint64_t connectorData;   /* maxColl x G x K x sliceBytes (Simple connectors)  */
+  uint64_t connectorFlags;  /* maxColl x G x 384 B (head, credit, direct line)   */
+  uint64_t llLines;         /* maxColl x G x K x 2 x llSliceBytes                */
+  uint64_t contexts;        /* maxColl x G x 128 B context buffer                */
+  uint64_t other;           /* SQ mirror, block state, stats, trace, ring table  */
+  uint64_t pinnedHost;      /* SQ, SQ cursors, CQ                                */
+  double perBlockPerColl;   /* device / (maxColl x G)                            */
+} occlFootprint_t;
+
 /* Bootstrap all-gather: gather `bytesPerRank` bytes from every rank into `out`
  * (rank-major).  Return 0 on success. */
 typedef int (*occlAllGatherFn)(const void* in, void* out, size_t bytesPerRank, void* ctx);
@@ -257,6 +270,7 @@ occlResult_t occlSetPriority(occlComm_t comm, int collId, int32_t priority);
 occlResult_t occlGetStats(occlComm_t comm, occlStats_t* out);
 occlResult_t occlGetCollStats(occlComm_t comm, int collId, occlCollStats_t* out);
 occlResult_t occlGetProbes(occlComm_t comm, occlProbes_t* out);
+occlResult_t occlGetFootprint(occlComm_t comm, occlFootprint_t* out);
 
 /* Device event trace of block `block` (cfg.traceCap > 0): the most recent
  * min(written, traceCap) records, oldest first, into out[0..cap); *n = count

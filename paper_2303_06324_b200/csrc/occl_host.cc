@@ -1099,6 +1099,25 @@ occlResult_t occlTraceReset(occlComm_t c) {
   return occlSuccess;
 }
 
+occlResult_t occlGetFootprint(occlComm_t c, occlFootprint_t* out) {
+  if (!c || !out) return occlInvalidArgument;
+  c = root_of(c);
+  const size_t M = c->cfg.maxColl, G = c->cfg.gridBlocks;
+  std::memset(out, 0, sizeof(*out));
+  out->connectorData = c->dataBytes;
+  out->connectorFlags = c->flagsBytes;
+  out->llLines = c->llBytes;
+  out->contexts = M * G * sizeof(CtxSlot);
+  out->other = c->cfg.sqDepth * sizeof(Sqe) + 3 * sizeof(uint64_t) + G * sizeof(BlockState) +
+               G * M * sizeof(uint32_t) + M * sizeof(uint32_t) + M * G * sizeof(CollStat) + G * sizeof(BlockStat) +
+               (size_t)G * c->cfg.traceCap * sizeof(TraceRec) + G * sizeof(uint32_t) +
+               (c->ringsDev ? kMaxRings * sizeof(RingDesc) : 0);
+  out->device = out->connectorData + out->connectorFlags + out->llLines + out->contexts + out->other;
+  out->pinnedHost = c->cfg.sqDepth * sizeof(Sqe) + G * sizeof(uint64_t) + M * sizeof(uint64_t);
+  out->perBlockPerColl = (double)(out->device) / (double)(M * G);
+  return occlSuccess;
+}
+
 occlResult_t occlSetPriority(occlComm_t c, int id, int32_t priority) {
   c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c || id < 0) return occlInvalidArgument;

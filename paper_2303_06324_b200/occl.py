@@ -37,7 +37,7 @@ EXPORTED = [
     "occlBroadcast", "occlWait", "occlTest", "occlSetCallback", "occlGetStats", "occlGetCollStats",
     "occlCommExit", "occlCommLaunch", "occlCommSetAutoLaunch", "occlCommQuiesce", "occlCommGetStream",
     "occlCollBlocks", "occlCommFuse", "occlGetProbes", "occlSetPriority", "occlGetTrace", "occlTraceReset",
-    "occlCommSplit", "occlReduce",
+    "occlCommSplit", "occlReduce", "occlGetFootprint",
 ]
 TRACE_EVENTS = {1: "fetch", 2: "switch_in", 3: "issue", 4: "publish", 5: "preempt", 6: "done", 7: "cqe",
                 8: "quit", 9: "exit", 10: "sdone", 11: "start", 12: "mark"}
@@ -69,6 +69,11 @@ class occlCollStats_t(C.Structure):
 
 class occlTraceRec_t(C.Structure):
     _fields_ = [("t", C.c_uint64), ("tag", C.c_uint32), ("arg", C.c_uint32)]
+
+
+class occlFootprint_t(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in ("device", "connectorData", "connectorFlags", "llLines", "contexts",
+                                          "other", "pinnedHost")] + [("perBlockPerColl", C.c_double)]
 
 
 class occlProbes_t(C.Structure):
@@ -112,6 +117,7 @@ def _lib():
             "occlReduceScatter": [vp, vp, sz, i, i, i, vp],
             "occlBroadcast": [vp, vp, sz, i, i, i, vp],
             "occlReduce": [vp, vp, sz, i, i, i, i, vp],
+            "occlGetFootprint": [vp, C.POINTER(occlFootprint_t)],
             "occlWait": [vp, i, i64],
             "occlTest": [vp, i, C.POINTER(i)],
             "occlSetCallback": [vp, i, CALLBACK, vp],
@@ -346,6 +352,11 @@ class Comm:
 
     def set_priority(self, coll_id, priority):
         check(_lib().occlSetPriority(self.h, coll_id, priority), "occlSetPriority")
+
+    def footprint(self) -> dict:
+        f = occlFootprint_t()
+        check(_lib().occlGetFootprint(self.h, C.byref(f)), "occlGetFootprint")
+        return {k: getattr(f, k) for k, _ in occlFootprint_t._fields_}
 
     def probes(self) -> dict:
         s = occlProbes_t()

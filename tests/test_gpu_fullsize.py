@@ -177,3 +177,21 @@ def test_occupancy_guard_refuses_non_resident_launch(occl_mod):
         assert e.value.code == occl_mod.occlCudaError
     finally:
         occl_mod.destroy_group(comms)                        # a sticky-errored comm can still be destroyed
+
+
+def test_memory_footprint_report(occl_mod):
+    """occlGetFootprint: the arena, flags, LL lines and contexts follow their
+    formulas (the paper's 4 MB per block for 1,000 collectives,
+    PAPER.md:581, is reading Q15)."""
+    comms = _ring(occl_mod, 2, maxColl=32)
+    try:
+        f = comms[0].footprint()
+        M, G, K, s = 32, BENCH["gridBlocks"], BENCH["connSlots"], BENCH["sliceBytes"]
+        assert f["connectorData"] == M * G * K * s
+        assert f["connectorFlags"] == M * G * 384
+        assert f["contexts"] == M * G * 128
+        assert f["llLines"] == M * G * K * 2 * comms[0].cfg.llSliceBytes
+        assert f["device"] == sum(f[k] for k in ("connectorData", "connectorFlags", "llLines", "contexts", "other"))
+        assert abs(f["perBlockPerColl"] - f["device"] / (M * G)) < 1
+    finally:
+        occl_mod.destroy_group(comms)
