@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--stages", type=int, default=5)
     ap.add_argument("--blocks-per-sm", type=int, default=1)
     ap.add_argument("--bulk-stores", type=int, default=0)
+    ap.add_argument("--direct-read", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--check", action="store_true", help="sampled oracle check of the timed output")
@@ -210,6 +211,7 @@ def make_ring(args, world, prank, dev, dist):
                                  prefetchSlices=args.prefetch, discardConsumed=args.discard,
                                  l2Hints=args.l2_hints, directMode=args.direct, stagingTiles=args.stages,
                                  blocksPerSM=args.blocks_per_sm, bulkStores=args.bulk_stores,
+                                 directRead=args.direct_read,
                                  maxColl=128, autoLaunch=0)
     hs = [occl.occlCommCreate(R, prank * V + i, dev, cfg) for i in range(V)]
     mine = [occl.occlCommGetHandle(h) for h in hs]

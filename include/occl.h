@@ -112,6 +112,7 @@ typedef struct {
   uint32_t llMaxBytes;    /* a collective whose per-block part is <= this uses LL (0 = never)   */
   uint32_t spinNs;        /* one spin = this many ns of failed polling (thresholds are in spins)  */
   int bulkStores;         /* 1 = staged tiles are stored with cp.async.bulk by the publisher lane  */
+  int directRead;         /* 1 = AR/RS first reduce step reads a same-process upstream's send buffer */
 } occlConfig_t;
 
 /* Aggregate counters (device counters summed over blocks/collectives). */

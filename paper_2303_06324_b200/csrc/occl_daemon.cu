@@ -184,7 +184,8 @@ template <int DT, int OP> __device__ __forceinline__ uint4 vop(const uint4& a, c
 enum : int { A_RECV = 1, A_REDUCE = 2, A_COPY = 4, A_SEND = 8,
              A_DIN = 16,    // direct receive: the upstream wrote the data into our recv buffer
              A_DOUT = 32,   // direct send: write into the downstream's recv buffer, not its connector
-             A_LL = 64 };   // LL protocol: 16-B lines {data, flag, data, flag}, no release fence
+             A_LL = 64,     // LL protocol: 16-B lines {data, flag, data, flag}, no release fence
+             A_DREAD = 128 }; // direct read: the input is the upstream's send buffer (no message)
 enum : int {
   P_SEND = A_SEND,
   P_RECV = A_RECV | A_COPY,
@@ -241,7 +242,7 @@ __device__ __forceinline__ void move_slice(const int prim, const char* src, cons
   typedef typename Elem<DT>::T T;
   constexpr int A = 16 / sizeof(T);
   constexpr int U = 2;                            // slices here are < kTmaMinBytes: 2 x 16 B per thread covers them
-  const bool recv = prim & A_RECV, reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
+  const bool recv = prim & (A_RECV | A_DREAD), reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
   const int n = (int)nelem;                       // <= sliceBytes / sizeof(T)
   if (n <= 0) return;
   const bool aligned = ((((uintptr_t)src) | ((uintptr_t)dst) | ((uintptr_t)cin) | ((uintptr_t)cout)) & 15) == 0;
@@ -344,8 +345,16 @@ __device__ __forceinline__ void step_prim(int kind, int n, int r, int root, int 
 // recv-buffer -> peer recv-buffer copy and the final Recv moves no data.  The
 // head / credit protocol is unchanged (a direct message still takes a connector
 // sequence number), so flow control and resume are exactly as before.
-__device__ __forceinline__ int directify(int prim, int kind, int n, int step, bool dOut, bool dIn) {
-  if (n == 1 || kind == kReduceScatter || kind == kReduce) return prim;   // partial sums are not final
+__device__ __forceinline__ int directify(int prim, int kind, int n, int step, bool dOut, bool dIn, bool dRead) {
+  if (n == 1) return prim;
+  // direct read: the first reduce step reads the upstream's send
+  // buffer itself, so the upstream's step 0 (copying it into our connector) and
+  // the message disappear on both ends of the edge
+  if (dRead && (kind == kAllReduce || kind == kReduceScatter)) {
+    if (step == 0 && dOut) return 0;                              // no-op: the downstream reads our buffer
+    if (step == 1 && dIn) prim = (prim & ~A_RECV) | A_DREAD;
+  }
+  if (kind == kReduceScatter || kind == kReduce) return prim;   // partial sums are not final
   const bool agPhase = kind != kAllReduce || step >= n - 1;    // data on the wire is final
   if (dOut && agPhase && (prim & A_SEND)) prim |= A_DOUT;
   const bool finalIn = kind != kAllReduce || step >= n;          // received data is final
@@ -515,6 +524,13 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched
   uint4* dst = reinterpret_cast<uint4*>(g);
 #pragma unroll
   for (int i = 0; i < kCtxBytes / 16; ++i) st_cg_v4(dst + i, w[i]);
+  if (p.directRead && R.directNext && n > 1 && !ll && (e.kind == kAllReduce || e.kind == kReduceScatter)) {
+    // tell the downstream where this submission's send buffer is (direct read)
+    char* f = R.flagsNext + ((size_t)c * G + b) * kFlagStride + kDirectOff + 16;
+    st_relaxed(f, e.sendbuff, p.sysScope);
+    if (p.sysScope) asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(f + 8), "l"(e.subSeq) : "memory");
+    else asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(f + 8), "l"(e.subSeq) : "memory");
+  }
   if (R.directPrev && n > 1 && e.kind != kReduceScatter && !ll) {
     // tell the upstream where this submission's final data goes (direct mode)
     char* f = R.flagsPrev + ((size_t)c * G + b) * kFlagStride + kDirectOff;
@@ -835,12 +851,15 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   char* connOut = R.dataNext + cb * K * p.sliceBytes;
   const char* directIn = p.flagsLocal + cb * kFlagStride + kDirectOff;   // {peer recvbuff, subSeq}
   const bool dOut = R.directNext != 0 && !ll, dIn = R.directPrev != 0 && !ll;
+  const bool dRead = p.directRead != 0;
+  const char* srcIn = p.flagsLocal + cb * kFlagStride + kDirectOff + 16;  // {upstream sendbuff, subSeq}
+  uint64_t peerSrc = 0;                                   // upstream's send buffer (direct read)
   const uint64_t subSeq = cx.s.subSeq;
   uint64_t peerRecv = 0;                                  // downstream's recv buffer (direct sends)
   bool prepared = false;                                  // pipe.ring[issued % D] holds the next slice
   const char* llLast = nullptr;                           // LL: last line of the next slice's input
   int curPrim = 0;
-  uint64_t doutOff = 0;
+  uint64_t doutOff = 0, dreadOff = 0;
   // ---- dynamic context -> registers
   Cursor dc{cx.d.loop, cx.d.step, cx.d.slc, cx.d.nsent, cx.d.nrecv};
   Cursor di = dc;
@@ -881,7 +900,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     if (!prepared) {
       int seg;
       step_prim(kind, n, r, root, di.step, inplace, curPrim, seg);
-      curPrim = directify(curPrim, kind, n, di.step, dOut, dIn);
+      curPrim = directify(curPrim, kind, n, di.step, dOut, dIn, dRead);
       uint64_t sendOff, recvOff, len;
       seg_geom(kind, n, r, count, segLen, seg, sendOff, recvOff, len);
       uint64_t laneHi = laneLo + part;
@@ -890,6 +909,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
       uint64_t hi = lo + E;
       if (hi > laneHi) hi = laneHi;
       doutOff = (recvOff + lo) * isz;
+      dreadOff = (sendOff + lo) * isz;
       sd.src = reinterpret_cast<const char*>(sendbuff) + (sendOff + lo) * isz;
       sd.dst = reinterpret_cast<char*>(recvbuff) + doutOff;
       sd.nelem = hi > lo ? (int64_t)(hi - lo) : 0;
@@ -933,6 +953,10 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
       creditSeen = ld_acquire(creditIn, sys);
       ok = di.nsent - creditSeen < (uint64_t)K;
     }
+    if (ok && (prim & A_DREAD) && peerSrc == 0) {         // the upstream admitted this submission?
+      if (ld_acquire(srcIn + 8, sys) == subSeq) peerSrc = ld_relaxed(srcIn, sys);
+      ok = peerSrc != 0;
+    }
     if (ok && (prim & A_DOUT) && peerRecv == 0) {         // the downstream admitted this submission?
       if (ld_acquire(directIn + 8, sys) == subSeq) peerRecv = ld_relaxed(directIn, sys);
       ok = peerRecv != 0;
@@ -955,6 +979,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     }
     spinStart = 0;
     if (prim & A_DOUT) sd.cout = reinterpret_cast<char*>(peerRecv) + doutOff;
+    if (prim & A_DREAD) sd.cin = reinterpret_cast<const char*>(peerSrc) + dreadOff;   // same layout as ours
     mbar_arrive(&pipe.full[issued % D]);
     trace_at(p, *m.tr, b, kEvIssue, sh.curId,
           (uint32_t)(di.nsent & 0x3fff) | ((uint32_t)(di.nrecv & 0x3fff) << 14) | ((uint32_t)(prim & 0xf) << 28));
@@ -972,7 +997,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
       }
       int pprim, pseg;
       step_prim(kind, n, r, root, dpf.step, inplace, pprim, pseg);
-      pprim = directify(pprim, kind, n, dpf.step, dOut, dIn);
+      pprim = directify(pprim, kind, n, dpf.step, dOut, dIn, dRead);
       if ((pprim & A_REDUCE) || !(pprim & A_RECV)) {      // primitive reads the send buffer
         uint64_t so, ro, ln;
         seg_geom(kind, n, r, count, segLen, pseg, so, ro, ln);
@@ -1088,10 +1113,11 @@ __device__ __forceinline__ uint4 lds_v4(const void* p) {
 // (connector slots always are; user buffers almost always).  Otherwise the
 // compute warps move it with register loads (move_slice).
 __device__ __forceinline__ int tma_vec_bytes(int dtype, int64_t nelem, const char* src, const char* dst,
-                                             const char* cout) {
+                                             const char* cout, const char* cin) {
   const int isz = elem_size(dtype);
   if (nelem <= 0) return 0;
-  if ((((uintptr_t)src) | ((uintptr_t)dst) | ((uintptr_t)cout)) & 15) return 0;   // cout: a peer buffer (direct)
+  // cout / cin may be peer buffers (direct send / direct read)
+  if ((((uintptr_t)src) | ((uintptr_t)dst) | ((uintptr_t)cout) | ((uintptr_t)cin)) & 15) return 0;
   const int vb = (int)((nelem * isz) & ~(int64_t)15);
   return vb >= kTmaMinBytes ? vb : 0;          // small slices: lower-latency register path
 }
@@ -1115,11 +1141,11 @@ __device__ __noinline__ void producer_main(const DaemonParams& p, Pipe& pipe, St
     if (sd.prim == P_EXIT) break;
     if (!(sd.prim & (A_COPY | A_SEND))) continue;     // direct final receive: data already in place
     if (sd.prim & A_LL) continue;                     // LL slices are moved by the compute warps alone
-    const int vb = tma_vec_bytes(sd.dtype, sd.nelem, sd.src, sd.dst, sd.cout);
+    const int vb = tma_vec_bytes(sd.dtype, sd.nelem, sd.src, sd.dst, sd.cout, sd.cin);
     if (vb == 0) continue;
     // order the acquire of the peer's head (generic proxy) before the bulk reads (async proxy)
     asm volatile("fence.proxy.async.global;" ::: "memory");
-    const bool recv = sd.prim & A_RECV, reduce = sd.prim & A_REDUCE;
+    const bool recv = sd.prim & (A_RECV | A_DREAD), reduce = sd.prim & A_REDUCE;
     const char* in = recv ? sd.cin : sd.src;
     for (int off = 0; off < vb; off += kTile) {
       const uint32_t s = cs;
@@ -1225,7 +1251,7 @@ template <int DT, int OP>
 __device__ __forceinline__ void tail_slice(const int prim, const char* src, const char* cin, char* dst, char* cout,
                                            int64_t e0, int64_t nelem, int tid, int nt) {
   typedef typename Elem<DT>::T T;
-  const bool rv = prim & A_RECV, rd = prim & A_REDUCE;
+  const bool rv = prim & (A_RECV | A_DREAD), rd = prim & A_REDUCE;
   const T* si = reinterpret_cast<const T*>(rv ? cin : src);
   const T* ss = reinterpret_cast<const T*>(src);
   for (int64_t e = e0 + tid; e < nelem; e += nt) {
@@ -1292,7 +1318,7 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
     char* dst = dp->dst;
     char* cout = dp->cout;
     const long long t1 = clock64();
-    const int vb = tma_vec_bytes(dtype, nelem, src, dst, cout);
+    const int vb = tma_vec_bytes(dtype, nelem, src, dst, cout, cin);
     const int op = dp->op;
     if (prim & A_LL) {
       const uint32_t inSeq = (uint32_t)dp->creditVal, outSeq = (uint32_t)dp->headVal;
@@ -1383,7 +1409,7 @@ __device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& 
       // the release fence then waits for no generic stores at all
       const SliceDesc& d = pipe.ring[i];
       const int vb = (d.prim & (A_COPY | A_SEND)) && !(d.prim & A_LL)
-                         ? tma_vec_bytes(d.dtype, d.nelem, d.src, d.dst, d.cout) : 0;
+                         ? tma_vec_bytes(d.dtype, d.nelem, d.src, d.dst, d.cout, d.cin) : 0;
       if (vb > 0) {
         bulkSlice = true;
         const bool copy = d.prim & A_COPY, send = d.prim & A_SEND;

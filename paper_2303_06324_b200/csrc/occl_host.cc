@@ -66,6 +66,7 @@ uint64_t fingerprint(const occlConfig_t& c) {
   mix(c.maxColl); mix(c.gridBlocks); mix(c.connSlots); mix(c.slicesPerChunk); mix(c.sliceBytes);
   mix(c.minBlockBytes);
   mix(c.directMode);
+  mix(c.directRead);
   mix(c.llSliceBytes);
   mix(c.llMaxBytes);
   return h;
@@ -496,6 +497,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->spinBoost = 2;
   c->spinCap = 65536;
   c->bulkStores = 0;
+  c->directRead = 1;
   c->spinNs = 150;                        // one spin ~ an L2 round trip of a flag poll under load (R1)
   c->stallLimit = 2;
   c->quitEnabled = 1;
@@ -735,6 +737,7 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   p.traceCap = c->cfg.traceCap;
   p.stages = c->cfg.stagingTiles;
   p.bulkStores = c->cfg.bulkStores;
+  p.directRead = c->cfg.directRead && c->cfg.directMode;
   p.blocksPerSM = c->cfg.blocksPerSM;
   p.l2Hints = c->cfg.l2Hints;
   Launcher* L = new Launcher();

@@ -11,7 +11,8 @@ enum Dtype : uint16_t { kI32 = 0, kF32 = 1, kBF16 = 2, kF16 = 3, kI64 = 4, kF64 
 
 constexpr int kMaxRanks = 64;
 constexpr int kFlagStride = 384;        // per (coll, block): head @+0, credit @+128, direct @+256 (own lines)
-constexpr int kDirectOff = 256;         // {u64 recvbuff, u64 subSeq} written by the downstream rank
+constexpr int kDirectOff = 256;         // {u64 recvbuff, u64 subSeq} written by the downstream rank,
+                                        // then {u64 sendbuff, u64 subSeq} written by the upstream (direct read)
 constexpr int kCtxBytes = 128;          // one context slot (static + dynamic), 16 B aligned
 constexpr int kMaxCacheWays = 32;
 
@@ -175,6 +176,7 @@ struct DaemonParams {
   uint32_t llMaxBytes;              // a collective uses LL when its per-block part is at most this
   int stages;                       // TMA staging tiles per block (x 2 x 16 KiB of shared memory)
   int bulkStores;                   // 1: staged tiles leave through cp.async.bulk stores (publisher lane)
+  int directRead;                   // 1: the first reduce step reads a same-process upstream's send buffer
   int blocksPerSM;                  // 1 or 2 co-resident daemon blocks per SM
   int l2Hints;                      // evict-first L2 policy for user-buffer loads / stores
 };

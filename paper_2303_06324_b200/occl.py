@@ -54,7 +54,7 @@ class occlConfig_t(C.Structure):
         ("pipeDepth", C.c_int), ("prefetchSlices", C.c_int), ("discardConsumed", C.c_int), ("l2Hints", C.c_int),
         ("directMode", C.c_int), ("stagingTiles", C.c_int), ("blocksPerSM", C.c_int), ("traceCap", C.c_uint32),
         ("llSliceBytes", C.c_uint32), ("llMaxBytes", C.c_uint32), ("spinNs", C.c_uint32),
-        ("bulkStores", C.c_int),
+        ("bulkStores", C.c_int), ("directRead", C.c_int),
     ]
 
 
