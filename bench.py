@@ -193,7 +193,10 @@ def setup_dist(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", init_method="env://")
+        # NCCL for the host-side plumbing (handle exchange, barriers, the max over
+        # ranks); OCCL_BENCH_BACKEND=gloo lets several processes share one GPU
+        # (the multi-process path smoke-tested on a single B200, tests/test_gpu_multiprocess.py)
+        dist.init_process_group(os.environ.get("OCCL_BENCH_BACKEND", "nccl"), init_method="env://")
     return world, rank, local, dist
 
 
@@ -229,12 +232,17 @@ def make_ring(args, world, prank, dev, dist):
     return comms, V
 
 
+def _red_dev(dist, dev):
+    """Device of the tensor used for the max-over-ranks reduction (gloo: host)."""
+    return dev if dist.get_backend() == "nccl" else "cpu"
+
+
 def run_occl(args):
     import torch
     from paper_2303_06324_b200 import occl
 
     world, prank, local, dist = setup_dist(args)
-    dev = local
+    dev = local % max(1, torch.cuda.device_count())   # one rank per GPU; several per GPU in the smoke test
     torch.cuda.set_device(dev)
     R = args.ranks
     size = int(args.size_mib * MiB)
@@ -302,7 +310,7 @@ def run_occl(args):
                      "publisher_fences": probes["nFence"],
                      "cycles_per_release_fence": round(probes["cycRelFence"] / max(1, probes["nFence"]), 1)}
     if dist is not None:
-        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms_total], dtype=torch.float64, device=_red_dev(dist, dev))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
@@ -358,7 +366,7 @@ def run_occl(args):
         barrier()
         te = (time.perf_counter() - t0) / e2e_steps
         if dist is not None:
-            t = torch.tensor([te], dtype=torch.float64, device=dev)
+            t = torch.tensor([te], dtype=torch.float64, device=_red_dev(dist, dev))
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
         e2e = {"value": busbw(size, R, te), "unit": "GB/s", "h2d_bytes_per_step": V * size,

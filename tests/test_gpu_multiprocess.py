@@ -1,0 +1,41 @@
+"""The multi-process path on one B200: several
+processes, each with its own communicator(s) and daemon kernel, connected through
+CUDA IPC with system-scope fences and connector-only edges between processes --
+the code path `bench.py --gpus N` uses across GPUs, exercised here with every
+process on the same device (the GPU time-slices the processes' daemons).
+
+* scripts/ipc_two_process.py: P processes x R/P fused ranks, every collective
+  kind bit-exact against the oracle (P = 2, 4, 8; P = 8 is the 8-GPU topology);
+* bench.py under torchrun with 2 processes (gloo plumbing): the N > 1 bench
+  path prints one valid JSON line with the max-over-ranks timing."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("world,ranks", [(2, 4), (4, 8), (8, 8)])
+def test_ipc_ring_across_processes(world, ranks):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ipc_two_process.py"), "--world", str(world),
+                        "--ranks", str(ranks)], capture_output=True, text=True, timeout=400, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("True") == world
+
+
+def test_bench_multiprocess_path():
+    env = dict(os.environ, OCCL_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--ranks", "8", "--size-mib", "8", "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu", "--check"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=400, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["check"]["bit_exact"]
+    assert d["config"]["ranks_per_gpu"] == 4
