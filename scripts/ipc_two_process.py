@@ -61,6 +61,30 @@ def worker(prank, world, ranks, port, q):
                 if not np.array_equal(U.to_np_bits(recvs[r]), exp[r]):
                     ok, msg = False, f"{kind} {dtype} rank {r} mismatch"
             msg += f" {kind}:{time.time() - t0:.2f}s"
+        # sub-communicators across processes: groups of non-neighbouring parent
+        # ranks (even / odd ranks), whose ring edges are IPC-opened on demand
+        groups = [list(range(0, ranks, 2)), list(range(1, ranks, 2))]
+        kids = []
+        for i, c in enumerate(comms):
+            r = prank * V + i
+            g = groups[r % 2]
+            kids.append((r, g, c.split(g)))
+        count = 30_001
+        xs = {}
+        for r, g, k in kids:
+            sends, recvs = U.make_bufs("allreduce", "f32", len(g), count, 99 + r % 2, 12)
+            xs[r] = (sends, recvs, g)
+            k.submit("allreduce", sends[g.index(r)], recvs[g.index(r)], 12, count, "f32")
+        for r, g, k in kids:
+            k.wait(12, 120)
+        for r, (sends, recvs, g) in xs.items():
+            exp = U.expected_full("allreduce", "f32", len(g), count, 99 + r % 2, 12)
+            if not np.array_equal(U.to_np_bits(recvs[g.index(r)]), exp[g.index(r)]):
+                ok, msg = False, f"split allreduce rank {r} mismatch"
+        msg += " split:ok"
+        dist.barrier()
+        for _, _, k in kids:
+            k.destroy()
         st = comms[0].stats()
         msg += f" launches={st['launches']} quits={st['quits']}"
         dist.barrier()
