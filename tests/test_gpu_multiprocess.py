@@ -5,9 +5,9 @@ the code path `bench.py --gpus N` uses across GPUs, exercised here with every
 process on the same device (the GPU time-slices the processes' daemons).
 
 * scripts/ipc_two_process.py: P processes x R/P fused ranks, every collective
-  kind and a sub-communicator split over non-neighbouring ranks (IPC-opened on
-  demand),
-  kind bit-exact against the oracle (P = 2, 4, 8; P = 8 is the 8-GPU topology);
+  kind bit-exact against the oracle, plus a sub-communicator split over
+  non-neighbouring ranks (IPC-opened on demand); P = 2, 4, 8 (8 = the 8-GPU
+  process topology);
 * bench.py under torchrun with 2 processes (gloo plumbing): the N > 1 bench
   path prints one valid JSON line with the max-over-ranks timing."""
 import json
