@@ -103,7 +103,7 @@ typedef struct {
   int pipeDepth;          /* slices in flight between the control warp and the data warps (1..8)   */
   int prefetchSlices;     /* send-buffer slices prefetched into L2 ahead of the issue cursor      */
   int discardConsumed;    /* 1 = drop consumed connector lines from L2 without write-back         */
-  int l2Hints;            /* 1 = evict-first L2 policy for send/recv-buffer streams               */
+  int l2Hints;            /* 1 = evict-first L2 policy for send/recv-buffer streams; 2 = also evict-last for connector stores */
   int directMode;         /* 1 = final data goes straight into a same-process peer's recv buffer  */
   int stagingTiles;       /* TMA staging ring depth per block (1..6), 32 KiB of shared memory each */
   int blocksPerSM;        /* 1 (up to 608 threads) or 2 (up to 384 threads, <= 3 staging tiles)    */

@@ -1077,6 +1077,11 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void st_cg_hint(void* p, const uint4& v, uint64_t pol) {
   asm volatile("st.global.cg.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;"
                :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
@@ -1167,8 +1172,11 @@ __device__ __noinline__ void producer_main(const DaemonParams& p, Pipe& pipe, St
 // downstream connector with 128-bit stores.
 template <int DT, int OP>
 __device__ __forceinline__ void consume_tile(const int prim, char* dst, char* cout, const Stage& s, int sz, int tid,
-                                             int nt, bool hints, uint64_t pol) {
+                                             int nt, bool hints, uint64_t pol, bool keep, uint64_t polKeep) {
   const bool reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
+  // l2Hints == 2: connector lines (re-read once by the downstream, then discarded)
+  // are stored evict-last so the streamed user buffers leave L2 before them
+  keep = keep && !(prim & A_DOUT);
   uint4* vd = reinterpret_cast<uint4*>(dst);
   uint4* vo = reinterpret_cast<uint4*>(cout);
   const int nv = sz >> 4;
@@ -1179,7 +1187,10 @@ __device__ __forceinline__ void consume_tile(const int prim, char* dst, char* co
       if (hints) st_cg_hint(vd + i, v, pol);
       else __stcg(vd + i, v);
     }
-    if (send) __stcg(vo + i, v);
+    if (send) {
+      if (keep) st_cg_hint(vo + i, v, polKeep);
+      else __stcg(vo + i, v);
+    }
   }
 }
 
@@ -1299,8 +1310,8 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
   const uint32_t D = (uint32_t)p.pipeDepth, S = (uint32_t)p.stages;
   const bool bulk = p.bulkStores != 0;
   const int lane = ctid & 31;
-  const bool hints = p.l2Hints != 0, discard = p.discardConsumed != 0;
-  const uint64_t pol = policy_evict_first();
+  const bool hints = p.l2Hints != 0, discard = p.discardConsumed != 0, keep = p.l2Hints == 2;
+  const uint64_t pol = policy_evict_first(), polKeep = policy_evict_last();
   const bool leader = ctid == 0;                       // probes
   unsigned long long cWait = 0, cData = 0, nData = 0;
   uint32_t cs = 0, cph = 0;                            // staging slot and its phase parity
@@ -1349,9 +1360,9 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
           continue;
         }
         if (prim & A_REDUCE) {
-          OCCL_DISPATCH(dtype, op, consume_tile, prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol);
+          OCCL_DISPATCH(dtype, op, consume_tile, prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol, keep, polKeep);
         } else {
-          consume_tile<kI32, kSum>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol);   // copy only
+          consume_tile<kI32, kSum>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol, keep, polKeep);   // copy only
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[s]);
