@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--pipe-depth", type=int, default=4)
     ap.add_argument("--prefetch", type=int, default=0)
     ap.add_argument("--discard", type=int, default=1)
-    ap.add_argument("--l2-hints", type=int, default=1)
+    ap.add_argument("--l2-hints", type=int, default=2)
     ap.add_argument("--direct", type=int, default=1)
     ap.add_argument("--stages", type=int, default=5)
     ap.add_argument("--blocks-per-sm", type=int, default=1)

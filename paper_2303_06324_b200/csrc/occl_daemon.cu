@@ -458,7 +458,7 @@ struct Pipe {
   SliceDesc ring[kMaxDepth];
   uint64_t full[kMaxDepth];      // control -> producer / compute / publisher: descriptor valid
   uint64_t sdone[kMaxDepth];     // compute warps -> publisher: slice moved (count = compute warps)
-  uint64_t empty[kMaxDepth];     // publisher -> control: slice moved AND published
+  uint64_t empty[kMaxDepth];     // publisher + producer -> control: slice published, descriptor read
   TraceCtl tr;                   // event-trace slot counter of this block
 };
 
@@ -1144,6 +1144,11 @@ __device__ __noinline__ void producer_main(const DaemonParams& p, Pipe& pipe, St
     mbar_wait(&pipe.full[j % D], (j / D) & 1);
     const SliceDesc sd = pipe.ring[j % D];
     if (sd.prim == P_EXIT) break;
+    // the descriptor is copied: the control thread may reuse its buffer.  Slices
+    // the producer does not stage (LL, register path, direct final receive) can
+    // complete without it, so without this arrive the control thread could
+    // rewrite ring[j % D] before this lane has read it
+    mbar_arrive(&pipe.empty[j % D]);
     if (!(sd.prim & (A_COPY | A_SEND))) continue;     // direct final receive: data already in place
     if (sd.prim & A_LL) continue;                     // LL slices are moved by the compute warps alone
     const int vb = tma_vec_bytes(sd.dtype, sd.nelem, sd.src, sd.dst, sd.cout, sd.cin);
@@ -1546,7 +1551,7 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
     for (uint32_t i = 0; i < D; ++i) {
       mbar_init(&pipe.full[i], 1);
       mbar_init(&pipe.sdone[i], nComputeWarps);
-      mbar_init(&pipe.empty[i], 1);
+      mbar_init(&pipe.empty[i], 2);     // publisher (slice published) + producer (descriptor read)
     }
     for (int i = 0; i < p.stages; ++i) {
       mbar_init(&tfull[i], 1);

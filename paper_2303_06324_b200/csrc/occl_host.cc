@@ -333,6 +333,7 @@ occlResult_t validate_config(const occlConfig_t& c) {
   if (c.pipeDepth < 1 || c.pipeDepth > 8) return occlInvalidArgument;
   if (c.prefetchSlices < 0 || c.prefetchSlices > 64) return occlInvalidArgument;
   if (c.stagingTiles < 1 || c.stagingTiles > 6) return occlInvalidArgument;
+  if (c.l2Hints < 0 || c.l2Hints > 2) return occlInvalidArgument;
   if (c.blocksPerSM < 1 || c.blocksPerSM > 2) return occlInvalidArgument;
   if (c.traceCap > (1u << 24)) return occlInvalidArgument;
   if (c.llSliceBytes < 8 || c.llSliceBytes % 8 || c.llSliceBytes > (1u << 20)) return occlInvalidArgument;
@@ -513,7 +514,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->llSliceBytes = 8 << 10;
   c->llMaxBytes = 64 << 10;
   c->blocksPerSM = 1;
-  c->l2Hints = 1;
+  c->l2Hints = 2;
   return occlSuccess;
 }
 

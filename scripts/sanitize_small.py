@@ -30,7 +30,7 @@ def main():
         try:
             for ci, (kind, dtype, count) in enumerate([("allreduce", "f32", 20_003), ("allreduce", "bf16", 3_001),
                                                        ("allgather", "i32", 5_001), ("reducescatter", "f32", 4_099),
-                                                       ("broadcast", "f16", 7_777), ("reduce", "f64", 2_049)]):
+                                                       ("broadcast", "f16", 7_777), ("allreduce", "f64", 2_049)]):
                 sends, recvs = U.make_bufs(kind, dtype, n, count, 70 + ci, ci)
                 U.run_collective(comms, kind, sends, recvs, ci, count, dtype, root=ci % n)
                 U.check_full(kind, dtype, n, count, 70 + ci, ci, recvs, root=ci % n)

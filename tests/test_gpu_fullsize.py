@@ -41,12 +41,13 @@ def _ring(occl_mod, n, **kw):
     return occl_mod.local_group(n, 0, **cfg)
 
 
-@pytest.mark.parametrize("direct,bulk", [(1, 0), (0, 0), (1, 1)])
-def test_bench_config_all_kinds_full_check(occl_mod, direct, bulk):
+@pytest.mark.parametrize("direct,bulk,hints", [(1, 0, 1), (0, 0, 1), (1, 1, 1), (1, 0, 2), (0, 0, 2)])
+def test_bench_config_all_kinds_full_check(occl_mod, direct, bulk, hints):
     """direct mode on / off; bulk-store mode (staged tiles leave through
-    cp.async.bulk stores issued by the publisher lane)."""
+    cp.async.bulk stores issued by the publisher lane); evict-last connector
+    stores (l2Hints=2)."""
     n = 8
-    comms = _ring(occl_mod, n, directMode=direct, bulkStores=bulk)
+    comms = _ring(occl_mod, n, directMode=direct, bulkStores=bulk, l2Hints=hints)
     try:
         for ci, (kind, dtype, count) in enumerate([("allreduce", "f32", 3_000_017), ("allreduce", "bf16", 2_500_003),
                                                    ("allreduce", "i32", 1_048_576), ("allgather", "f32", 400_009),
