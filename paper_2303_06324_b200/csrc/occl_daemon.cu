@@ -458,7 +458,7 @@ struct Pipe {
   SliceDesc ring[kMaxDepth];
   uint64_t full[kMaxDepth];      // control -> producer / compute / publisher: descriptor valid
   uint64_t sdone[kMaxDepth];     // compute warps -> publisher: slice moved (count = compute warps)
-  uint64_t empty[kMaxDepth];     // publisher + producer -> control: slice published, descriptor read
+  uint64_t empty[kMaxDepth];     // publisher + producer + compute -> control: slice published, descriptor read
   TraceCtl tr;                   // event-trace slot counter of this block
 };
 
@@ -1324,20 +1324,32 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
     const uint32_t i = j % D;
     const long long t0 = clock64();
     mbar_wait(&pipe.full[i], (j / D) & 1);
-    const SliceDesc* dp = &pipe.ring[i];
-    const int prim = dp->prim;
+    // lane 0 reads the descriptor and broadcasts it: the warp's only reader of
+    // ring[i] is then the lane that hands it back on empty[i] (direct ordering)
+    int prim = 0, dtype = 0, op = 0;
+    uint32_t inSeq = 0, outSeq = 0;
+    unsigned long long nel = 0, a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    if (lane == 0) {
+      const SliceDesc* dp = &pipe.ring[i];
+      prim = dp->prim; dtype = dp->dtype; op = dp->op;
+      inSeq = (uint32_t)dp->creditVal; outSeq = (uint32_t)dp->headVal;
+      nel = (unsigned long long)dp->nelem;
+      a0 = (uintptr_t)dp->src; a1 = (uintptr_t)dp->cin; a2 = (uintptr_t)dp->dst; a3 = (uintptr_t)dp->cout;
+    }
+    prim = __shfl_sync(0xffffffffu, prim, 0);
     if (prim == P_EXIT) break;
-    const int dtype = dp->dtype;
-    const int64_t nelem = dp->nelem;
-    const char* src = dp->src;
-    const char* cin = dp->cin;
-    char* dst = dp->dst;
-    char* cout = dp->cout;
+    dtype = __shfl_sync(0xffffffffu, dtype, 0);
+    op = __shfl_sync(0xffffffffu, op, 0);
+    inSeq = __shfl_sync(0xffffffffu, inSeq, 0);
+    outSeq = __shfl_sync(0xffffffffu, outSeq, 0);
+    const int64_t nelem = (int64_t)__shfl_sync(0xffffffffu, nel, 0);
+    const char* src = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, a0, 0));
+    const char* cin = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, a1, 0));
+    char* dst = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, a2, 0));
+    char* cout = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, a3, 0));
     const long long t1 = clock64();
     const int vb = tma_vec_bytes(dtype, nelem, src, dst, cout, cin);
-    const int op = dp->op;
     if (prim & A_LL) {
-      const uint32_t inSeq = (uint32_t)dp->creditVal, outSeq = (uint32_t)dp->headVal;
       OCCL_DISPATCH(dtype, op, ll_slice, prim, src, cin, dst, cout, nelem, inSeq, outSeq, ctid, cnt);
     } else if (!(prim & (A_COPY | A_SEND))) {
       // direct final receive: the data is already in place, nothing to move
@@ -1379,7 +1391,10 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
     // this warp's stores (ordered by __syncwarp) are released to the publisher,
     // which fences once and raises the peers' flags (publisher_main)
     __syncwarp();
-    if (lane == 0) mbar_arrive(&pipe.sdone[i]);
+    if (lane == 0) {
+      mbar_arrive(&pipe.sdone[i]);
+      mbar_arrive(&pipe.empty[i]);                   // this warp is done with ring[i] too
+    }
     if (leader) {
       const long long t2 = clock64();
       cWait += t1 - t0;
@@ -1551,7 +1566,9 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
     for (uint32_t i = 0; i < D; ++i) {
       mbar_init(&pipe.full[i], 1);
       mbar_init(&pipe.sdone[i], nComputeWarps);
-      mbar_init(&pipe.empty[i], 2);     // publisher (slice published) + producer (descriptor read)
+      // publisher (slice published) + producer + compute warps (descriptor read):
+      // every reader of ring[i] releases it directly to the control thread
+      mbar_init(&pipe.empty[i], 2 + nComputeWarps);
     }
     for (int i = 0; i < p.stages; ++i) {
       mbar_init(&tfull[i], 1);
