@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "i32"])
     ap.add_argument("--grid-blocks", type=int, default=18)
     ap.add_argument("--slice-kib", type=int, default=192)
-    ap.add_argument("--conn-slots", type=int, default=4)
+    ap.add_argument("--conn-slots", type=int, default=5)
     ap.add_argument("--slices-per-chunk", type=int, default=2)
     ap.add_argument("--threads", type=int, default=608)
     ap.add_argument("--pipe-depth", type=int, default=4)
@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--discard", type=int, default=1)
     ap.add_argument("--l2-hints", type=int, default=2)
     ap.add_argument("--direct", type=int, default=1)
-    ap.add_argument("--stages", type=int, default=5)
+    ap.add_argument("--stages", type=int, default=6)
     ap.add_argument("--blocks-per-sm", type=int, default=1)
     ap.add_argument("--bulk-stores", type=int, default=0)
     ap.add_argument("--direct-read", type=int, default=1)
@@ -389,7 +389,8 @@ def run_occl(args):
         if os.path.exists(tf):
             try:
                 d = json.load(open(tf))
-                key = f"{R}x{args.size_mib:g}MiB-{args.dtype}-G{args.grid_blocks}-s{args.slice_kib}k"
+                key = (f"{R}x{args.size_mib:g}MiB-{args.dtype}-G{args.grid_blocks}-s{args.slice_kib}k"
+                       f"-K{args.conn_slots}-st{args.stages}-h{args.l2_hints}")
                 if key in d:
                     traffic = d[key]["dram_bytes_per_step"] * (args.steps / launches)
             except Exception:

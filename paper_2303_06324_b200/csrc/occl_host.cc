@@ -510,7 +510,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->prefetchSlices = 0;
   c->discardConsumed = 1;
   c->directMode = 1;
-  c->stagingTiles = 5;
+  c->stagingTiles = 6;
   c->llSliceBytes = 8 << 10;
   c->llMaxBytes = 64 << 10;
   c->blocksPerSM = 1;

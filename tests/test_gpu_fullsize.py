@@ -1,5 +1,5 @@
 """GPU parity in the launch configuration bench.py times (SURVEY.md §8(c),
-DESIGN.md §4): 192 KiB slices through a 5-stage TMA staging ring, publisher lane,
+DESIGN.md §4): 192 KiB slices through a 6-stage TMA staging ring, 5 connector slots, publisher lane,
 direct mode, L2 discard / evict-first hints -- the data path the headline
 number comes from -- plus its variants and guards.
 
@@ -22,8 +22,8 @@ pytestmark = pytest.mark.gpu
 
 import gpu_util as U  # noqa: E402
 
-BENCH = dict(gridBlocks=18, sliceBytes=192 << 10, connSlots=4, slicesPerChunk=2, blockThreads=608, pipeDepth=4,
-             stagingTiles=5, maxColl=16)
+BENCH = dict(gridBlocks=18, sliceBytes=192 << 10, connSlots=5, slicesPerChunk=2, blockThreads=608, pipeDepth=4,
+             stagingTiles=6, maxColl=16)
 
 
 @pytest.fixture(scope="module")
