@@ -32,11 +32,13 @@ def main():
     ap.add_argument("--kinds", default="allreduce,allgather,reducescatter,broadcast")
     ap.add_argument("--out", default="gpurun_out/c2_sweep")
     ap.add_argument("--grid-blocks", type=int, default=18)
+    ap.add_argument("--conn-slots", type=int, default=5, help="connector slots K (bench configuration: 5)")
     ap.add_argument("--ll-max", type=int, default=64 << 10, help="LL protocol threshold (per-block part bytes)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     n = args.ranks
-    comms = harness.ring(n, 0, gridBlocks=args.grid_blocks, maxColl=128, autoLaunch=0, llMaxBytes=args.ll_max)
+    comms = harness.ring(n, 0, gridBlocks=args.grid_blocks, maxColl=128, autoLaunch=0, llMaxBytes=args.ll_max,
+                         connSlots=args.conn_slots)
     rows = []
     sizes = []
     s = args.min_bytes
