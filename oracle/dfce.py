@@ -388,6 +388,12 @@ class Simulator:
         ent = L.cache.get(way)
         if ent is not None and ent[0] == coll:
             return ent[1]
+        if ent is not None and ent[1].progressed:
+            # the way holds another collective's context that progressed since its
+            # last save: it is switched out here, so the lazy save happens now
+            # (PAPER.md:513-514).  Reached when an admission under the priority
+            # policy moves the lane's position between two micro-steps of a run.
+            self._save_ctx(r, b, ent[0], ent[1])
         d = R.dyn_global[(coll, b)].copy()
         self.loads += 1
         L.cache[way] = (coll, d)

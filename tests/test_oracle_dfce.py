@@ -399,3 +399,20 @@ def test_subcommunicators_baseline_deadlocks_on_cyclic_orders():
     _check_sub_results(sim, bufs, metas, n)
     sim, bufs = dfce.run_orders(metas, cyclic, dfce.SimConfig(seed=1, **_BF_CFG), seed=2)   # OCCL: fine
     _check_sub_results(sim, bufs, metas, n)
+
+
+@pytest.mark.parametrize("ways", [1, 2, 4])
+def test_cache_conflict_eviction_saves_progressed_context(ways):
+    """A direct-mapped way shared by two collectives (ids 0 and 4 at 4 ways), the
+    priority policy admitting new SQEs between micro-steps of a run: the context
+    switched out of the way must be saved lazily, else it
+    resumes from stale progress and the ranks' slices disagree.  Found by timing
+    O2 on a scaled C3 (scripts/oracle_timing.py)."""
+    spec = [("broadcast", "f32", 509, 1), ("reducescatter", "f32", 204, 0), ("broadcast", "f32", 10108, 7),
+            ("reducescatter", "bf16", 2085, 0), ("allreduce", "bf16", 1118, 0)]
+    metas = [dfce.CollMeta(i, *s) for i, s in enumerate(spec)]
+    cfg = dfce.SimConfig(order_policy="priority", cache_ways=ways, seed=1)
+    sim, bufs = dfce.run_orders(metas, [[4, 0, 1, 2, 3]] * 8, cfg, seed=3)
+    _check_results(sim, bufs, metas, 8)
+    _check_accounting(sim, metas, 8)
+    assert sim.saves >= 1
