@@ -1381,8 +1381,9 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
         } else {
           consume_tile<kI32, kSum>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol, keep, polKeep);   // copy only
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[s]);
+        // every lane releases its own reads of the tile to the producer's next TMA
+        // load into it (direct ordering; measured free vs one elected lane)
+        mbar_arrive(&tempty[s]);
       }
       // ragged tail (< 16 B) straight from global memory
       const int64_t e0 = vb / elem_size(dtype);
@@ -1572,7 +1573,8 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
     }
     for (int i = 0; i < p.stages; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], p.bulkStores ? 1 : nComputeWarps);   // bulk mode: the storing lane frees stages
+      // every compute lane frees a stage; bulk mode: the storing lane does
+      mbar_init(&tempty[i], p.bulkStores ? 1 : 32 * nComputeWarps);
       mbar_init(&tred[i], nComputeWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
