@@ -1,12 +1,21 @@
 #!/usr/bin/env python
 """Benchmark: all-reduce bus bandwidth of the OCCL daemon path on B200.
 
-Workload (BASELINE.json configs[1], the C2 sweep's headline point): a ring of
-R = 8 ranks (--ranks) all-reducing S = 256 MiB (--size-mib) of fp32 per rank,
-sum, out of place.  The 8 ranks are spread over the N GPUs of the job: each GPU
-hosts R/N ranks (virtual ranks sharing HBM, served by ONE fused daemon launch);
-at N = 8 every rank is its own B200 and the ring runs over NVLink (IPC).  Total
-work is fixed as N grows ("scaling": "strong").
+Workload (BASELINE.json configs[1], the C2 sweep's headline point): an
+all-reduce of S = 256 MiB (--size-mib) of fp32 per rank, sum, out of place.
+
+* N = 1 (default): a ring of R = 8 virtual ranks (--ranks) on the one B200,
+  served by ONE fused daemon launch (they share HBM).  Also reported: the
+  same ring on the connector-only / system-scope data path a one-process-per-
+  GPU ring runs (forceSysScope = 1), key "connector_only".
+* N >= 2 (torchrun): one rank per GPU (R = N), one process each, connected
+  with occlCommInit over torch.distributed and CUDA IPC; the ring crosses
+  NVLink.  Sizes --sizes (MiB) are swept; beside OCCL, the SAME all-reduce
+  through NCCL on the same GPUs (torch.distributed): NCCL_ALGO=Ring
+  NCCL_PROTO=Simple (the paper's algorithm, the graded ratio) and NCCL's
+  default choice (context).  NVML NVLink TX/RX byte deltas are OCCL's own
+  evidence that the ring spans the GPUs.  Per-GPU work is fixed as N grows
+  ("scaling": "weak").
 
 A step = one all-reduce on every rank.  K steps are submitted to the SQ (one
 SQE per rank per step, distinct collective ids) with an Exiting SQE, then the
@@ -14,7 +23,8 @@ daemon is launched once; the timed region is bracketed by CUDA events on the
 daemon's stream (plus barrier + synchronize on both sides).  Inputs (8 x 256
 MiB = 2 GiB) are larger than L2.
 
-value = nccl-tests bus bandwidth busbw = S * 2(R-1)/R / t_step   (GB/s, 1e9)
+value = nccl-tests bus bandwidth busbw = S * 2(R-1)/R / t_step   (GB/s, 1e9;
+the metric BASELINE.json names, a per-rank figure by nccl-tests convention).
 
 --impl reference times the CPU oracle (oracle/ring.py, the plain numpy ring
 fold) on a bounded sample of the same workload on this box's host cores.
@@ -44,7 +54,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="occl", choices=["occl", "reference"])
     ap.add_argument("--size-mib", type=float, default=256.0)
-    ap.add_argument("--ranks", type=int, default=8)
+    ap.add_argument("--ranks", type=int, default=0, help="ring size; default 8 at N=1, N (one per GPU) at N>1")
+    ap.add_argument("--sizes", default="64,256,1024", help="N>1: MiB per rank swept (the --size-mib point is the headline)")
+    ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--no-conn-only", action="store_true")
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "i32"])
     ap.add_argument("--grid-blocks", type=int, default=18)
     ap.add_argument("--slice-kib", type=int, default=192)
@@ -196,11 +209,50 @@ def setup_dist(args):
         # NCCL for the host-side plumbing (handle exchange, barriers, the max over
         # ranks); OCCL_BENCH_BACKEND=gloo lets several processes share one GPU
         # (the multi-process path smoke-tested on a single B200, tests/test_gpu_multiprocess.py)
+        # NCCL's Ring/Simple protocol for the default group: it is the baseline
+        # arm (the paper's algorithm); the OCCL data plane never uses NCCL
+        os.environ.setdefault("NCCL_ALGO", "Ring")
+        os.environ.setdefault("NCCL_PROTO", "Simple")
         dist.init_process_group(os.environ.get("OCCL_BENCH_BACKEND", "nccl"), init_method="env://")
     return world, rank, local, dist
 
 
-def make_ring(args, world, prank, dev, dist):
+def bench_cfg(args, **extra):
+    from paper_2303_06324_b200 import occl
+    kw = dict(gridBlocks=args.grid_blocks, sliceBytes=args.slice_kib * 1024, connSlots=args.conn_slots,
+              slicesPerChunk=args.slices_per_chunk, blockThreads=args.threads, pipeDepth=args.pipe_depth,
+              prefetchSlices=args.prefetch, discardConsumed=args.discard, l2Hints=args.l2_hints,
+              directMode=args.direct, stagingTiles=args.stages, blocksPerSM=args.blocks_per_sm,
+              bulkStores=args.bulk_stores, directRead=args.direct_read, maxColl=128, autoLaunch=0)
+    kw.update(extra)
+    return occl.occlConfigDefault(**kw)
+
+
+def timed_launch(comms, sends, recvs, nsteps, stream, first_id=0, barrier=None):
+    """nsteps all-reduces per local rank (distinct ids), an Exiting SQE, ONE daemon
+    launch (serving every local rank); returns device ms (CUDA events on the
+    daemon's stream)."""
+    import torch
+    ids = [(first_id + k) % 120 for k in range(nsteps)]
+    for i, c in enumerate(comms):
+        for cid in ids:
+            c.all_reduce(sends[i], recvs[i], cid)
+        c.exit()
+    if barrier is not None:
+        barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    comms[0].launch()                      # one fused launch serves all local ranks
+    e1.record(stream)
+    for c in comms:
+        for cid in set(ids):
+            c.wait(cid, 600)
+    comms[0].quiesce(600)
+    e1.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def make_ring(args, world, prank, dev, dist, **extra):
     """R ranks over `world` processes, V = R/world consecutive ranks per process;
     handles exchanged over torch.distributed; local ranks fused into one daemon."""
     from paper_2303_06324_b200 import occl
@@ -208,14 +260,7 @@ def make_ring(args, world, prank, dev, dist):
     if R % world:
         raise SystemExit("--ranks must be a multiple of the GPU count")
     V = R // world
-    cfg = occl.occlConfigDefault(gridBlocks=args.grid_blocks, sliceBytes=args.slice_kib * 1024,
-                                 connSlots=args.conn_slots, slicesPerChunk=args.slices_per_chunk,
-                                 blockThreads=args.threads, pipeDepth=args.pipe_depth,
-                                 prefetchSlices=args.prefetch, discardConsumed=args.discard,
-                                 l2Hints=args.l2_hints, directMode=args.direct, stagingTiles=args.stages,
-                                 blocksPerSM=args.blocks_per_sm, bulkStores=args.bulk_stores,
-                                 directRead=args.direct_read,
-                                 maxColl=128, autoLaunch=0)
+    cfg = bench_cfg(args, **extra)
     hs = [occl.occlCommCreate(R, prank * V + i, dev, cfg) for i in range(V)]
     mine = [occl.occlCommGetHandle(h) for h in hs]
     if dist is not None:
@@ -238,10 +283,17 @@ def _red_dev(dist, dev):
 
 
 def run_occl(args):
+    world, prank, local, dist = setup_dist(args)
+    if world > 1 and (args.ranks in (0, world)):
+        return run_multi(args, world, prank, local, dist)
+    if not args.ranks:
+        args.ranks = 8
+    return run_single(args, world, prank, local, dist)
+
+
+def run_single(args, world, prank, local, dist):
     import torch
     from paper_2303_06324_b200 import occl
-
-    world, prank, local, dist = setup_dist(args)
     dev = local % max(1, torch.cuda.device_count())   # one rank per GPU; several per GPU in the smoke test
     torch.cuda.set_device(dev)
     R = args.ranks
@@ -263,21 +315,7 @@ def run_occl(args):
 
     def run_steps(nsteps, first_id=0):
         """nsteps all-reduces per rank in ONE daemon launch; returns device ms."""
-        ids = [(first_id + k) % 120 for k in range(nsteps)]
-        for i, c in enumerate(comms):
-            for cid in ids:
-                c.all_reduce(sends[i], recvs[i], cid)
-            c.exit()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        comms[0].launch()                      # one fused launch serves all V local ranks
-        e1.record(stream)
-        for c in comms:
-            for cid in set(ids):
-                c.wait(cid, 600)
-        comms[0].quiesce(600)
-        e1.synchronize()
-        return e0.elapsed_time(e1)
+        return timed_launch(comms, sends, recvs, nsteps, stream, first_id)
 
     steps_per_launch = 100
     # warm-up (untimed)
@@ -435,11 +473,206 @@ def run_occl(args):
     }
     if check is not None:
         line["check"] = check
+    occl.destroy_group(comms)
+    if world == 1 and not args.no_conn_only:
+        co = conn_only_variant(args, dev, sends, recvs, size, peaks)
+        co["vs_direct_mode"] = co["value"] / value
+        line["connector_only"] = co
     if prank == 0:
         print(json.dumps(line))
-    occl.destroy_group(comms)
     if dist is not None:
         dist.destroy_process_group()
+    return 0
+
+
+def conn_only_variant(args, dev, sends, recvs, size, peaks):
+    """The same ring on the data path a one-process-per-GPU ring runs: every
+    edge connector-only (no direct mode / direct read) with system-scope
+    fences and flags (forceSysScope = 1) -- VERDICT r01 next #4."""
+    import torch
+    from paper_2303_06324_b200 import occl
+    R = args.ranks
+    comms, V = make_ring(args, 1, 0, dev, None, forceSysScope=1)
+    stream = torch.cuda.ExternalStream(comms[0].stream(), device=dev)
+    try:
+        timed_launch(comms, sends, recvs, max(3, args.warmup), stream)
+        steps = max(5, args.steps)
+        ms = timed_launch(comms, sends, recvs, steps, stream, first_id=50) / steps
+    finally:
+        occl.destroy_group(comms)
+    bw = busbw(size, R, ms / 1e3)
+    alg = 2 * size * V / (ms / 1e3) / 1e9
+    peak = peaks.get("hbm_gbs", 6650.0)
+    return {"value": bw, "unit": "GB/s", "ms_per_step": ms, "steps": steps,
+            "config": "forceSysScope=1: connector-only edges, .sys fences / flags (directMode, directRead off)",
+            "roofline_frac": alg / peak, "vs_direct_mode": None}
+
+
+# ============================================================================ N >= 2: one rank per GPU
+class NvlinkCounters:
+    """NVML NVLink data TX/RX byte counters of this process's GPU (best effort)."""
+
+    def __init__(self, dev):
+        self.ok = False
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N, self.h = N, N.nvmlDeviceGetHandleByIndex(dev)
+            self.fields = [N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX]
+            self.read()
+            self.ok = True
+        except Exception:
+            pass
+
+    def read(self):
+        N = self.N
+        vals = N.nvmlDeviceGetFieldValues(self.h, self.fields)
+        out = []
+        for v in vals:
+            if v.nvmlReturn != 0:
+                raise RuntimeError("nvlink field unsupported")
+            out.append(int(v.value.ullVal) * 1024)          # KiB counters
+        return out
+
+    def delta(self, fn):
+        if not self.ok:
+            return fn(), None
+        try:
+            a = self.read()
+        except Exception:
+            return fn(), None
+        r = fn()
+        try:
+            b = self.read()
+        except Exception:
+            return r, None
+        return r, {"tx_bytes": b[0] - a[0], "rx_bytes": b[1] - a[1]}
+
+
+def nccl_allreduce_ms(dist, group, t, steps, warmup):
+    """Same-box NCCL all-reduce (torch.distributed), CUDA events on torch's stream."""
+    import torch
+    for _ in range(warmup):
+        dist.all_reduce(t, group=group)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        dist.all_reduce(t, group=group)
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def run_multi(args, world, prank, local, dist):
+    """One rank per GPU: the metric's own configuration at N = 2 / 4 / 8."""
+    import torch
+    from paper_2303_06324_b200 import occl
+    ndev = max(1, torch.cuda.device_count())
+    dev = local % ndev
+    torch.cuda.set_device(dev)
+    R = world
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16, "i32": torch.int32}[args.dtype]
+    item = torch.tensor([], dtype=tdt).element_size()
+    sizes = sorted({float(x) for x in args.sizes.split(",") if x} | {args.size_mib})
+    comm = occl.process_group(device=dev, cfg=bench_cfg(args))       # occlCommInit over torch.distributed
+    stream = torch.cuda.ExternalStream(comm.stream(), device=dev)
+    backend = dist.get_backend()
+    distinct = ndev >= world                                         # NCCL needs one GPU per rank
+    nccl_ok = backend == "nccl" and distinct and not args.no_nccl
+    nccl_groups = {}
+    if nccl_ok:
+        # the default process group was created with NCCL_ALGO=Ring NCCL_PROTO=Simple (main());
+        # a second group gets NCCL's own algorithm choice (communicators are created lazily)
+        nccl_groups["ring_simple"] = None
+        saved = {k: os.environ.pop(k) for k in ("NCCL_ALGO", "NCCL_PROTO") if k in os.environ}
+        nccl_groups["default"] = dist.new_group(backend="nccl")
+        t = torch.ones(1024, device=dev)
+        dist.all_reduce(t, group=nccl_groups["default"])           # create it now, without the env
+        torch.cuda.synchronize()
+        os.environ.update(saved)
+    nvl = NvlinkCounters(dev)
+    peaks = measured_peaks()
+    rows = []
+    with ClockSampler(dev) as clk:
+        for smib in sizes:
+            size = int(smib * MiB)
+            count = size // item
+            send = torch.empty(count, dtype=tdt, device=dev)
+            recv = torch.empty(count, dtype=tdt, device=dev)
+            occl.test_fill(send, args.dtype, 1, 0, prank)
+            torch.cuda.synchronize()
+            timed_launch([comm], [send], [recv], max(3, args.warmup), stream, barrier=dist.barrier)
+            ms_occl, nv = nvl.delta(lambda: timed_launch([comm], [send], [recv], args.steps, stream, first_id=10,
+                                                         barrier=dist.barrier))
+            t = torch.tensor([ms_occl], dtype=torch.float64, device=_red_dev(dist, dev))
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item()) / args.steps
+            row = {"size_bytes": size, "occl_ms": ms, "occl_busbw": busbw(size, R, ms / 1e3),
+                   "nvlink_counters": nv}
+            if args.check and smib == args.size_mib:
+                import numpy as np
+                from oracle import ring
+                rng = np.random.default_rng(0)
+                idx = np.unique(np.concatenate([rng.integers(0, count, 20000), [0, count - 1]]))
+                got = recv[torch.from_numpy(idx).to(dev)].cpu()
+                got = got.view(torch.int16).numpy().view(np.uint16) if args.dtype == "bf16" else got.numpy().view(np.uint32)
+                exp = ring.expected_at("allreduce", args.dtype, R, count, 1, 0, idx)
+                exp = exp.view(np.uint16) if args.dtype == "bf16" else exp.view(np.uint32)
+                row["check"] = {"sampled_elements": int(len(idx)), "bit_exact": bool(np.array_equal(got, exp))}
+            for name, g in nccl_groups.items():
+                x = recv.clone()
+                m = nccl_allreduce_ms(dist, g, x, args.steps, max(3, args.warmup))
+                tt = torch.tensor([m], dtype=torch.float64, device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                m = float(tt.item())
+                row[f"nccl_{name}_ms"] = m
+                row[f"nccl_{name}_busbw"] = busbw(size, R, m / 1e3)
+                del x
+            rows.append(row)
+            del send, recv
+            torch.cuda.empty_cache()
+    head = [r for r in rows if r["size_bytes"] == int(args.size_mib * MiB)][0]
+    size = head["size_bytes"]
+    ms_step = head["occl_ms"]
+    value = head["occl_busbw"]
+    egress = size * 2 * (R - 1) / R                                 # NVLink bytes per GPU per all-reduce
+    achieved = egress / (ms_step / 1e3) / 1e9
+    roofline = {"bound": "nvlink", "achieved": achieved, "peak": 770.0, "unit": "GB/s", "frac": achieved / 770.0,
+                "traffic": (head["nvlink_counters"] or {}).get("tx_bytes", None) and
+                head["nvlink_counters"]["tx_bytes"] / args.steps,
+                "peak_source": "measured peer copy 770 GB/s per direction (B200_PROFILING.md; 900 nominal)",
+                "algorithmic_bytes_per_step": egress}
+    baseline = {}
+    for name in nccl_groups:
+        baseline[f"nccl_{name}"] = {"value": head[f"nccl_{name}_busbw"], "ms_per_step": head[f"nccl_{name}_ms"]}
+    ge64 = [r for r in rows if r["size_bytes"] >= 64 * MiB and "nccl_ring_simple_busbw" in r]
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic (counter-based hash generator, inputs resident in HBM)",
+        "config": {"workload": f"C2 allreduce, {R}-rank ring, one rank per GPU, {args.size_mib:g} MiB/rank "
+                               f"{args.dtype} sum", "ranks": R, "ranks_per_gpu": 1, "size_bytes_per_rank": size,
+                   "grid_blocks": args.grid_blocks, "slice_bytes": args.slice_kib * 1024,
+                   "conn_slots": args.conn_slots, "backend_plumbing": backend,
+                   "l2": "inputs of 64 MiB-1 GiB per GPU; L2 not flushed between steps"},
+        "gpu_launches": 1,
+        "clocks": clk.summary(),
+        "roofline": roofline,
+        "cpu_baseline": None,
+        "e2e": None,
+        "baseline": baseline or {"nccl": "unavailable: " + ("backend " + backend if backend != "nccl" else
+                                                            "fewer GPUs than ranks" if not distinct else "--no-nccl")},
+        "ratio_vs_nccl": (value / head["nccl_ring_simple_busbw"]) if "nccl_ring_simple_busbw" in head else None,
+        "ratio_vs_nccl_ge64MiB_min": min((r["occl_busbw"] / r["nccl_ring_simple_busbw"] for r in ge64), default=None),
+        "sweep": rows,
+    }
+    if prank == 0:
+        print(json.dumps(line))
+    comm.destroy()
+    dist.destroy_process_group()
     return 0
 
 

@@ -32,6 +32,9 @@
  *     Mismatched metadata across ranks is undefined behaviour.  An id may be
  *     resubmitted (with new buffers) only after it completed locally
  *     (PAPER.md:382-383); resubmitting an in-flight id returns occlDuplicateSubmit.
+ *     Local completion means this rank's buffers are free: no peer reads `send`
+ *     or writes `recv` of that submission any more (a direct-reading downstream
+ *     acknowledges its last read before the CQE is posted).
  *   - In-place (NCCL conventions): send == recv (AllReduce, Broadcast);
  *     send == recv + rank*sendcount (AllGather); recv == send + rank*recvcount
  *     (ReduceScatter).
@@ -113,6 +116,11 @@ typedef struct {
   uint32_t spinNs;        /* one spin = this many ns of failed polling (thresholds are in spins)  */
   int bulkStores;         /* 1 = staged tiles are stored with cp.async.bulk by the publisher lane  */
   int directRead;         /* 1 = AR/RS first reduce step reads a same-process upstream's send buffer */
+  uint64_t stallNs;       /* FIFO fetch gate: 0 = an entry is stuck after stallLimit preemptions without
+                             progress; > 0 = also when no queued entry progressed for this long (reading R3) */
+  int forceSysScope;      /* 1 = treat every peer as another process (CUDA IPC): system-scope fences,
+                             connector-only edges (no direct mode / direct read) -- the one-process-per-GPU
+                             data path, selectable on one device for testing and benchmarking */
 } occlConfig_t;
 
 /* Aggregate counters (device counters summed over blocks/collectives). */
@@ -222,10 +230,14 @@ occlResult_t occlCommFuse(occlComm_t* comms, int n);
  * sets).  `members` lists the parent ranks of the new ring in its rank order;
  * every member calls this with the same list (globally agreed, like collId) and
  * the caller must be a member.  The child shares the parent's daemon, SQ, CQ and
- * collId registry (an id belongs to one communicator at a time); its collectives
- * use dedicated connectors at (collId, block) in the members' arenas, opened from
- * the handles the parent received at occlCommConnect.  Destroy children before
- * their parent.  Up to 31 splits per communicator. */
+ * collId registry; its collectives use dedicated connectors at (collId, block)
+ * in the members' arenas, opened from the handles the parent received at
+ * occlCommConnect.  A collId is BOUND to the (sub-)communicator of its first
+ * submission -- its connector sequence numbers belong to that ring's edges --
+ * and submitting it on another returns occlInvalidUsage; destroying a child
+ * retires the ids bound to it.  Destroy children before their parent.  Up to
+ * 31 live sub-communicators per communicator (a destroyed child's slot is
+ * reused). */
 occlResult_t occlCommSplit(occlComm_t parent, int nmembers, const int* members, occlComm_t* child);
 
 /* Create + GetHandle + ag(...) + Connect.  The paper's occlCommInit. */

@@ -157,3 +157,24 @@ def pairwise_reversed_orders(nranks: int, k: int):
     """PAPER.md:737 'different orders pairwise' read as adjacent rank pairs reversed
     (SPEC.md:548): even ranks ascending, odd ranks descending."""
     return [list(range(k)) if r % 2 == 0 else list(reversed(range(k))) for r in range(nranks)]
+
+
+def arrival_delays(nranks: int, nitems: int, mean_s: float, seed: int):
+    """Per-rank inter-arrival gaps (seconds) ~ Exp(mean_s), independent per rank:
+    rank r waits delays[r][k] before its k-th submission (C3 / C4 live arrival,
+    VERDICT r01 next #2).  Seeded; pure data."""
+    out = []
+    for r in range(nranks):
+        rng = random.Random((seed * 1_000_003) ^ (0x5DEECE66D * (r + 1)))
+        out.append([rng.expovariate(1.0 / mean_s) if mean_s > 0 else 0.0 for _ in range(nitems)])
+    return out
+
+
+def iteration_orders(nranks: int, nitems: int, seed: int, iteration: int):
+    """Independent random per-rank permutation for one DP iteration (C4)."""
+    orders = []
+    for r in range(nranks):
+        o = list(range(nitems))
+        random.Random((seed << 20) ^ (iteration << 8) ^ r).shuffle(o)
+        orders.append(o)
+    return orders

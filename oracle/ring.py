@@ -30,7 +30,10 @@ Indices are mod n.  (+) is the collective's reducing function (PAPER.md:306
   f16  : RNE_f16(float32(a) op float32(b))   (same argument, 24 >= 2*11 + 2)
   i64  : two's-complement wrap (sum, prod), signed max / min
   f64  : IEEE-754 binary64, round-to-nearest-even (numpy float64)
-  max / min are exact (no rounding); inputs carry no NaN.
+  max / min are exact (no rounding); -0 < +0 (IEEE 754-2019 maximum / minimum,
+  reading R24); their inputs carry no NaN.  Sums may meet +-Inf and produce
+  NaN (Inf + -Inf); NaN payloads are unspecified by IEEE 754, so tests compare
+  NaN results by class, every other result bit for bit.
 
 Where the paper is silent (segment map, operand order, bf16 partial precision)
 the readings are SURVEY.md §8(c) Q6/Q7, listed in DESIGN.md.
@@ -59,6 +62,24 @@ def bf16_to_f32(b: np.ndarray) -> np.ndarray:
     return (np.asarray(b, dtype=np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32)
 
 
+def ieee_max(x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """IEEE 754-2019 maximum of non-NaN operands (reading R24): the
+    larger value, where -0 compares less than +0 (so max(-0, +0) = +0 in either
+    operand order; numpy's np.maximum returns its first operand on ties)."""
+    x, y = np.asarray(x), np.asarray(y)
+    r = np.where(x > y, x, y)
+    z = (x == 0) & (y == 0)
+    return np.where(z, np.where(np.signbit(x) & np.signbit(y), x, np.abs(x)), r)
+
+
+def ieee_min(x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """IEEE 754-2019 minimum of non-NaN operands (reading R24): -0 < +0."""
+    x, y = np.asarray(x), np.asarray(y)
+    r = np.where(x < y, x, y)
+    z = (x == 0) & (y == 0)
+    return np.where(z, np.where(np.signbit(x) | np.signbit(y), -np.abs(x), np.abs(x)), r)
+
+
 def _f32_op(x: np.ndarray, y: np.ndarray, op: str) -> np.ndarray:
     """The reducing function on float32 operands (IEEE, round to nearest even)."""
     if op == "sum":
@@ -66,9 +87,9 @@ def _f32_op(x: np.ndarray, y: np.ndarray, op: str) -> np.ndarray:
     if op == "prod":
         return (x * y).astype(np.float32)
     if op == "max":
-        return np.maximum(x, y)
+        return ieee_max(x, y)
     if op == "min":
-        return np.minimum(x, y)
+        return ieee_min(x, y)
     raise ValueError(op)
 
 
@@ -108,7 +129,7 @@ def add(a: np.ndarray, b: np.ndarray, dtype: str, op: str = "sum") -> np.ndarray
             return x + y
         if op == "prod":
             return x * y
-        return np.maximum(x, y) if op == "max" else np.minimum(x, y)
+        return ieee_max(x, y) if op == "max" else ieee_min(x, y)
     raise ValueError(dtype)
 
 

@@ -109,12 +109,29 @@ __device__ __forceinline__ T ld_cg_scalar(const T* p) {
 // correctly rounded 16-bit result (__hadd2 / __hmul2 / __hmax2 / __hmin2).
 enum : int { kSum = 0, kProd = 1, kMax = 2, kMin = 3 };
 
+// max / min are IEEE 754-2019 maximum / minimum (reading R24): -0 < +0
+// whatever the operand order, so a ring fold of signed zeros is order-free.  For
+// two zeros the result's sign bit is the AND (max) / OR (min) of theirs.
 template <int OP> __device__ __forceinline__ uint32_t op_f32(uint32_t a, uint32_t b) {
   const float x = __uint_as_float(a), y = __uint_as_float(b);
   if constexpr (OP == kSum) return __float_as_uint(__fadd_rn(x, y));
   else if constexpr (OP == kProd) return __float_as_uint(__fmul_rn(x, y));
-  else if constexpr (OP == kMax) return __float_as_uint(fmaxf(x, y));
-  else return __float_as_uint(fminf(x, y));
+  else if constexpr (OP == kMax) return ((a | b) << 1) == 0 ? (a & b) : __float_as_uint(fmaxf(x, y));
+  else return ((a | b) << 1) == 0 ? (a | b) : __float_as_uint(fminf(x, y));
+}
+// signed-zero rule of max / min on the two 16-bit lanes of a packed word
+template <int OP> __device__ __forceinline__ uint32_t zero_fix16(uint32_t r, uint32_t a, uint32_t b) {
+  if constexpr (OP == kMax || OP == kMin) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t sh = 16u * h, ah = (a >> sh) & 0xffffu, bh = (b >> sh) & 0xffffu;
+      if (((ah | bh) & 0x7fffu) == 0) {
+        const uint32_t v = OP == kMax ? (ah & bh) : (ah | bh);
+        r = (r & ~(0xffffu << sh)) | (v << sh);
+      }
+    }
+  }
+  return r;
 }
 template <int OP> __device__ __forceinline__ uint32_t op_i32(uint32_t a, uint32_t b) {
   if constexpr (OP == kSum) return a + b;
@@ -130,7 +147,7 @@ template <int OP> __device__ __forceinline__ uint32_t op_bf16x2(uint32_t a, uint
   else if constexpr (OP == kProd) z = __hmul2(x, y);
   else if constexpr (OP == kMax) z = __hmax2(x, y);
   else z = __hmin2(x, y);
-  return *reinterpret_cast<uint32_t*>(&z);
+  return zero_fix16<OP>(*reinterpret_cast<uint32_t*>(&z), a, b);
 }
 template <int OP> __device__ __forceinline__ uint32_t op_f16x2(uint32_t a, uint32_t b) {
   const __half2 x = *reinterpret_cast<const __half2*>(&a);
@@ -140,7 +157,7 @@ template <int OP> __device__ __forceinline__ uint32_t op_f16x2(uint32_t a, uint3
   else if constexpr (OP == kProd) z = __hmul2(x, y);
   else if constexpr (OP == kMax) z = __hmax2(x, y);
   else z = __hmin2(x, y);
-  return *reinterpret_cast<uint32_t*>(&z);
+  return zero_fix16<OP>(*reinterpret_cast<uint32_t*>(&z), a, b);
 }
 template <int OP> __device__ __forceinline__ uint64_t op_i64(uint64_t a, uint64_t b) {
   if constexpr (OP == kSum) return a + b;
@@ -153,8 +170,8 @@ template <int OP> __device__ __forceinline__ uint64_t op_f64(uint64_t a, uint64_
   double z;
   if constexpr (OP == kSum) z = __dadd_rn(x, y);
   else if constexpr (OP == kProd) z = __dmul_rn(x, y);
-  else if constexpr (OP == kMax) z = fmax(x, y);
-  else z = fmin(x, y);
+  else if constexpr (OP == kMax) { if (((a | b) << 1) == 0) return a & b; z = fmax(x, y); }
+  else { if (((a | b) << 1) == 0) return a | b; z = fmin(x, y); }
   return (uint64_t)__double_as_longlong(z);
 }
 template <int DT, int OP> __device__ __forceinline__ uint64_t op_d(uint64_t a, uint64_t b) {
@@ -432,6 +449,7 @@ constexpr int kRoleWarps = 3;          // warps 0..2: control, producer, publish
 constexpr int kTile = 16384;           // TMA staging tile (bytes per operand)
 constexpr int kMaxStages = 6;          // staging ring depth: up to 6 x 2 x 16 KiB of loads in flight
 constexpr int kTmaMinBytes = 16384;    // slices below this use register loads (latency-bound sizes)
+constexpr uint32_t kQuitLatch = 0x80000000u;   // quitWord: every block of the launch voted to quit
 
 // Scheduler state of one block; touched only by the control thread.
 struct Sched {
@@ -439,6 +457,8 @@ struct Sched {
   uint64_t T;
   uint32_t qlen, pos, exiting;
   uint32_t rr;                 // priority policy: next non-front entry to visit
+  uint32_t voted;              // this block voted for the launch's voluntary quit
+  uint64_t lastProgress;       // %globaltimer of the last run that committed a slice
   int lastRun, curId;
   int way;
   unsigned long long cycRun, cycPoll, cycAcqFence, cycRelFence, nCommit;   // probes
@@ -706,6 +726,10 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
   const uint32_t qlen = sh.qlen;
   bool allStalled = qlen > 0;
   for (uint32_t i = 0; i < qlen && allStalled; ++i) allStalled = (m.tq[i] >> 16) >= p.stallLimit;
+  // reading R3, time-based variant: "cannot progress for a long time" = no queued
+  // entry committed a slice for stallNs (and the current front was preempted)
+  if (!allStalled && qlen > 0 && p.stallNs && (m.tq[sh.pos] >> 16) > 0 && now - sh.lastProgress > p.stallNs)
+    allStalled = true;
   // -- fetch an SQE, gated by the order policy
   const bool canFetch = !sh.exiting && qlen < (uint32_t)p.maxColl &&
                         (qlen == 0 || (p.orderPolicy == 0 ? allStalled : (sh.iter % (uint64_t)p.priorityCadence) == 0));
@@ -746,12 +770,43 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
     if (fetched) return CMD_NONE;
   }
   const bool stuck = qlen == 0 || allStalled;
+  // Voluntary quit is decided for the whole launch: a block
+  // that has been stuck or idle for quitIdleNs only VOTES; the launch quits once
+  // every block voted (a block gone alone would strand the SQEs of its lanes --
+  // and cap the SQ mirror with its stale cursor -- until its siblings quit too).
+  // quitWord = votes | kQuitLatch; the latch is set by a CAS from exactly
+  // quitTotal votes, and a vote is withdrawn only by a CAS that sees no latch,
+  // so once latched every block leaves.  A block that consumed the Exiting SQE
+  // keeps its vote.
+  bool quitNow = false;
+  if (p.quitEnabled && !(qlen == 0 && sh.exiting)) {
+    const bool eligible = stuck && now - sh.lastFetch > p.quitIdleNs;
+    if (eligible && !sh.voted) {
+      atomicAdd(p.quitWord, 1u);
+      sh.voted = 1;
+    } else if (!eligible && sh.voted) {
+      uint32_t w = *(volatile uint32_t*)p.quitWord;
+      for (;;) {
+        if (w & kQuitLatch) { quitNow = true; break; }
+        const uint32_t o = atomicCAS(p.quitWord, w, w - 1);
+        if (o == w) { sh.voted = 0; break; }
+        w = o;
+      }
+    }
+    if (sh.voted && !quitNow) {
+      const uint32_t w = *(volatile uint32_t*)p.quitWord;
+      quitNow = (w & kQuitLatch) ||
+                (w == p.quitTotal && atomicCAS(p.quitWord, w, w | kQuitLatch) == w);
+    }
+  }
   if (qlen == 0 && sh.exiting) {
     sh.exiting = 0;
+    if (!sh.voted && p.quitWord) atomicAdd(p.quitWord, 1u);
+    sh.voted = 1;
     p.blkStats[b].exits++;
     trace_at(p, *m.tr, b, kEvExit, 0, 0);
     cmd = CMD_EXIT;
-  } else if (stuck && p.quitEnabled && now - sh.lastFetch > p.quitIdleNs) {
+  } else if (quitNow) {
     p.blkStats[b].quits++;                           // voluntary quit
     trace_at(p, *m.tr, b, kEvQuit, 0, 0);
     cmd = CMD_EXIT;
@@ -853,6 +908,19 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   const bool dOut = R.directNext != 0 && !ll, dIn = R.directPrev != 0 && !ll;
   const bool dRead = p.directRead != 0;
   const char* srcIn = p.flagsLocal + cb * kFlagStride + kDirectOff + 16;  // {upstream sendbuff, subSeq}
+  // Read-done acknowledgement of direct read (reduce-scatter).  An RS rank's own
+  // completion does not depend on its downstream's progress: when its last
+  // loop's sends fit in the connector ((n-2) * spc <= K) it could post its CQE
+  // -- and its caller rewrite the send buffer or resubmit the id -- while the
+  // downstream has not yet read that buffer.  So the downstream raises `ack` in
+  // our flag line (+32) to the submission number once it committed its last
+  // direct-read slice, and we hold RUN_DONE until then (a failed ack poll is a
+  // spin: preemptible like any connector wait).  An all-reduce needs no ack:
+  // its final Recv carries data the downstream produced after its direct read.
+  const bool dreadUp = dRead && dOut && n > 1 && kind == kReduceScatter;     // downstream reads our buffer
+  const bool dreadDown = dRead && dIn && n > 1 && kind == kReduceScatter;    // we read our upstream's
+  const char* ackIn = p.flagsLocal + cb * kFlagStride + kDirectOff + 32;
+  char* ackOut = R.flagsPrev + cb * kFlagStride + kDirectOff + 32;
   uint64_t peerSrc = 0;                                   // upstream's send buffer (direct read)
   const uint64_t subSeq = cx.s.subSeq;
   uint64_t peerRecv = 0;                                  // downstream's recv buffer (direct sends)
@@ -874,12 +942,22 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   unsigned long long nSlices = 0, cPoll = 0;
   const long long tRun = clock64();
   trace_at(p, *m.tr, b, kEvSwitchIn, sh.curId, sh.pos);
+  // commit one slice the data warps finished (in order); the downstream side of
+  // a reduce-scatter direct read acknowledges its last direct-read slice
+  auto commit = [&](uint32_t slot) {
+    const int cp = pipe.ring[slot].prim;
+    if (dreadDown && (cp & A_DREAD) && dc.loop + 1 == nloops && dc.slc + 1 == (uint32_t)spc) {
+      if (sys) asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(ackOut), "l"(subSeq) : "memory");
+      else asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(ackOut), "l"(subSeq) : "memory");
+    }
+    advance(dc, cp, spc, nsteps);
+  };
   int run;
   for (;;) {
     // ---- slices the data warps moved and published: advance the committed cursor
     if (committed != issued && mbar_test(&pipe.empty[committed % D], (committed / D) & 1)) {
       do {
-        advance(dc, pipe.ring[committed % D].prim, spc, nsteps);
+        commit(committed % D);
         ++committed;
         ++nSlices;
       } while (committed != issued && mbar_test(&pipe.empty[committed % D], (committed / D) & 1));
@@ -890,7 +968,12 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
       m.tq[sh.pos] &= 0xffffu;                            // progressed: not stalled
     }
     if (di.loop >= nloops) {                              // everything issued
-      if (committed == issued) { run = RUN_DONE; break; }
+      if (committed != issued) continue;
+      if (!dreadUp || ld_acquire(ackIn, sys) == subSeq) { run = RUN_DONE; break; }
+      // the downstream has not finished reading our send buffer: a failed poll
+      const uint64_t now = globaltimer();
+      if (spinStart == 0) spinStart = now;
+      if (now - spinStart > T * spinNs) { run = RUN_PREEMPT; break; }   // pipe already drained
       continue;
     }
     if (issued - committed == D) continue;                // every buffer busy
@@ -968,7 +1051,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
       if (now - spinStart > T * spinNs) {                // two-phase blocking: preempt
         while (committed != issued) {                    // drain the pipe
           mbar_wait(&pipe.empty[committed % D], (committed / D) & 1);
-          advance(dc, pipe.ring[committed % D].prim, spc, nsteps);
+          commit(committed % D);
           ++committed;
           ++nSlices;
         }
@@ -1022,6 +1105,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   cx.d.loop = dc.loop; cx.d.step = (uint16_t)dc.step; cx.d.slc = (uint16_t)dc.slc;
   cx.d.nsent = dc.nsent; cx.d.nrecv = dc.nrecv;
   sh.T = T;
+  if (nSlices) sh.lastProgress = globaltimer();
   sh.cycRun += clock64() - tRun;
   sh.cycPoll += cPoll;
   sh.nCommit += nSlices;
@@ -1551,6 +1635,8 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
     sh.exiting = bs.exiting;
     sh.iter = 0;
     sh.rr = 1;
+    sh.voted = 0;
+    sh.lastProgress = 0;
     sh.lastRun = -1;
     sh.curId = -1;
     sh.cycRun = sh.cycPoll = sh.cycAcqFence = sh.cycRelFence = sh.nCommit = 0;

@@ -67,6 +67,7 @@ uint64_t fingerprint(const occlConfig_t& c) {
   mix(c.minBlockBytes);
   mix(c.directMode);
   mix(c.directRead);
+  mix(c.forceSysScope);
   mix(c.llSliceBytes);
   mix(c.llMaxBytes);
   return h;
@@ -96,6 +97,7 @@ struct Launcher {
   std::atomic<int> autoLaunch{1};
   std::atomic<int> sticky{0};
   int quitUploaded = -1;                         // effective quitEnabled in paramsDev
+  uint32_t* quitWord = nullptr;                  // device: the launch's voluntary-quit votes (zeroed per launch)
   int lastLaunchQuit = 0;                        // the current/last launch may quit voluntarily
 };
 }  // namespace occl
@@ -125,8 +127,11 @@ struct occlComm {
   uint64_t* cqDev = nullptr;
   std::atomic<uint64_t> sqTail{0};
   // per-collective host state
-  std::vector<uint64_t> subSeq;
-  std::unique_ptr<std::atomic<int>[]> state;     // 0 idle, 1 in flight
+  // per collId: submission token = subSeq << 1 | in-flight bit.  Completion
+  // CASes the exact token it observed, so a completion can never be applied to
+  // a newer submission of the same id (wait + resubmit racing the poller).
+  std::unique_ptr<std::atomic<uint64_t>[]> tok;
+  std::vector<int> boundSub;                     // root: ring each collId is bound to (-1 free, -2 retired)
   std::vector<occlCallback_t> cb;
   std::vector<void*> cbArg;
   std::vector<int32_t> prio;                     // per-collective priority (default: collId)
@@ -151,6 +156,7 @@ struct occlComm {
   std::vector<char> peerIpc;                     // root: 1 if opened through CUDA IPC
   RingDesc* ringsDev = nullptr;                  // root: [kMaxRings]
   int nrings = 0;
+  std::vector<int> freeRings;                    // root: ring slots of destroyed sub-communicators
   int children = 0;                              // root: live sub-communicators
   std::vector<occlComm*> owner;                  // root: per collId, the comm that submitted it
 };
@@ -218,6 +224,10 @@ occlResult_t launch_locked(Launcher* L) {
         cudaSuccess) { L->sticky.store((int)e); return occlCudaError; }
     L->quitUploaded = quit;
   }
+  if ((e = cudaMemsetAsync(L->quitWord, 0, sizeof(uint32_t), L->stream)) != cudaSuccess) {
+    L->sticky.store((int)e);
+    return occlCudaError;
+  }
   if ((e = cudaEventRecord(L->evStart, L->stream)) != cudaSuccess) { L->sticky.store((int)e); return occlCudaError; }
   int r = occl_internal_launch_daemon(&c0->params, L->paramsDev, (int)L->members.size(), c0->cfg.blockThreads,
                                       L->stream);
@@ -229,12 +239,17 @@ occlResult_t launch_locked(Launcher* L) {
   return occlSuccess;
 }
 
+inline bool tok_inflight(uint64_t t) { return (t & 1) != 0; }
+inline uint64_t tok_seq(uint64_t t) { return t >> 1; }
+
 bool try_complete(occlComm* c, int id) {
-  if (c->state[id].load(std::memory_order_acquire) != 1) return false;
+  uint64_t t = c->tok[id].load(std::memory_order_acquire);
+  if (!tok_inflight(t)) return false;
   const uint64_t done = reinterpret_cast<volatile uint64_t*>(c->cqHost)[id];
-  if (done < c->subSeq[id]) return false;
-  int one = 1;
-  if (!c->state[id].compare_exchange_strong(one, 0)) return false;
+  if (done < tok_seq(t)) return false;
+  // complete exactly the submission observed: fails if the id was completed and
+  // resubmitted in between (ABA between the poller and occlWait)
+  if (!c->tok[id].compare_exchange_strong(t, t & ~1ull)) return false;
   c->inflight.fetch_sub(1);
   if (!c->owner.empty() && c->owner[id] && c->owner[id] != c) c->owner[id]->inflight.fetch_sub(1);
   occlCallback_t f = c->cb[id];
@@ -269,7 +284,7 @@ void supervisor_main(Launcher* L) {
     }
     for (occlComm* c : ms)
       for (int id = 0; id < c->cfg.maxColl && c->inflight.load() > 0; ++id)
-        if (c->cb[id] && c->state[id].load() == 1) try_complete(c, id);
+        if (c->cb[id] && tok_inflight(c->tok[id].load())) try_complete(c, id);
     if (!pending) {
       std::unique_lock<std::mutex> lk(L->mu);
       L->cv.wait_for(lk, std::chrono::milliseconds(5));
@@ -283,8 +298,14 @@ occlResult_t launcher_start(Launcher* L, const std::vector<occlComm*>& members) 
   L->dev = members[0]->dev;
   L->members = members;
   cudaSetDevice(L->dev);
+  if (cudaMalloc(&L->quitWord, sizeof(uint32_t)) != cudaSuccess) return occlCudaError;
+  if (cudaMemset(L->quitWord, 0, sizeof(uint32_t)) != cudaSuccess) return occlCudaError;
   std::vector<DaemonParams> ps;
-  for (occlComm* c : members) ps.push_back(c->params);
+  for (occlComm* c : members) {
+    c->params.quitWord = L->quitWord;
+    c->params.quitTotal = (uint32_t)(c->cfg.gridBlocks * members.size());
+    ps.push_back(c->params);
+  }
   if (cudaMalloc(&L->paramsDev, ps.size() * sizeof(DaemonParams)) != cudaSuccess) return occlCudaError;
   if (cudaMemcpy(L->paramsDev, ps.data(), ps.size() * sizeof(DaemonParams), cudaMemcpyHostToDevice) != cudaSuccess)
     return occlCudaError;
@@ -309,6 +330,7 @@ void launcher_stop(Launcher* L) {
   cudaSetDevice(L->dev);
   if (L->launched) cudaEventSynchronize(L->evDone);
   if (L->paramsDev) cudaFree(L->paramsDev);
+  if (L->quitWord) cudaFree(L->quitWord);
   if (L->evStart) cudaEventDestroy(L->evStart);
   if (L->evDone) cudaEventDestroy(L->evDone);
   if (L->stream) cudaStreamDestroy(L->stream);
@@ -402,16 +424,23 @@ occlResult_t submit(occlComm* sc, int kind, int dtype, int op, int root, size_t 
   if (op < occlSum || op > occlMin) return occlInvalidArgument;
   if ((kind == kBroadcast || kind == kReduce) && (root < 0 || root >= sc->nranks)) return occlInvalidArgument;
   if (count > 0 && (!send || !recv)) return occlInvalidArgument;
-  if (c->state[collId].load() == 1 && !try_complete(c, collId)) return occlDuplicateSubmit;
-  c->subSeq[collId]++;
+  if (tok_inflight(c->tok[collId].load()) && !try_complete(c, collId)) return occlDuplicateSubmit;
+  // a collId is bound to the ring of its first submission: its connector head /
+  // credit counters are per (collId, block) on each member, so moving the id to
+  // another rank set would pair counters of different edges
+  int& bound = c->boundSub[collId];
+  if (bound == -1) bound = sc->sub;
+  else if (bound != sc->sub) return occlInvalidUsage;
+  const uint64_t seq = tok_seq(c->tok[collId].load()) + 1;
   if (count == 0) {                                   // completes at submission (reading Q18)
-    reinterpret_cast<volatile uint64_t*>(c->cqHost)[collId] = c->subSeq[collId];
+    reinterpret_cast<volatile uint64_t*>(c->cqHost)[collId] = seq;
+    c->tok[collId].store(seq << 1, std::memory_order_release);
     if (c->cb[collId]) c->cb[collId](collId, c->cbArg[collId]);
     return occlSuccess;
   }
   Sqe e{};
   e.sub = (uint16_t)sc->sub;
-  e.subSeq = c->subSeq[collId];
+  e.subSeq = seq;
   e.count = count;
   e.sendbuff = (uint64_t)(uintptr_t)send;
   e.recvbuff = (uint64_t)(uintptr_t)recv;
@@ -424,7 +453,7 @@ occlResult_t submit(occlComm* sc, int kind, int dtype, int op, int root, size_t 
   e.priority = c->prio[collId];
   c->owner[collId] = sc;
   if (sc != c) sc->inflight.fetch_add(1);
-  c->state[collId].store(1, std::memory_order_release);
+  c->tok[collId].store((seq << 1) | 1, std::memory_order_release);
   c->inflight.fetch_add(1);
   return push_sqe(c, e, true);
 }
@@ -536,9 +565,9 @@ occlResult_t occlCommCreate(occlComm_t* out, int nranks, int rank, int cudaDev, 
   c->dataBytes = M * G * cfg.connSlots * cfg.sliceBytes;
   c->flagsBytes = M * G * kFlagStride;
   c->llBytes = M * G * cfg.connSlots * 2ull * cfg.llSliceBytes;
-  c->subSeq.assign(M, 0);
-  c->state.reset(new std::atomic<int>[M]);
-  for (size_t i = 0; i < M; ++i) c->state[i].store(0);
+  c->tok.reset(new std::atomic<uint64_t>[M]);
+  for (size_t i = 0; i < M; ++i) c->tok[i].store(0);
+  c->boundSub.assign(M, -1);
   c->cb.assign(M, nullptr);
   c->cbArg.assign(M, nullptr);
   c->prio.resize(M);
@@ -659,7 +688,7 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   } else if ((r = open(hs[prev], &c->prevArena, &c->prevIpc)) != occlSuccess) {
     return r;
   }
-  c->sysScope = local ? 0 : 1;
+  c->sysScope = (local && !c->cfg.forceSysScope) ? 0 : 1;
   c->peerArena[next] = c->nextArena;
   c->peerIpc[next] = c->nextIpc;
   if (prev != next) {
@@ -676,8 +705,8 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   rd.flagsPrev = c->prevArena + hs[prev].flagsOffset;
   rd.nranks = c->nranks;
   rd.rank = c->rank;
-  rd.directNext = c->cfg.directMode && !c->nextIpc;
-  rd.directPrev = c->cfg.directMode && !c->prevIpc;
+  rd.directNext = c->cfg.directMode && !c->nextIpc && !c->cfg.forceSysScope;
+  rd.directPrev = c->cfg.directMode && !c->prevIpc && !c->cfg.forceSysScope;
   if (cudaMalloc(&c->ringsDev, kMaxRings * sizeof(RingDesc)) != cudaSuccess) return occlCudaError;
   if (cudaMemcpy(c->ringsDev, &rd, sizeof(rd), cudaMemcpyHostToDevice) != cudaSuccess) return occlCudaError;
   c->nrings = 1;
@@ -727,8 +756,8 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   p.discardConsumed = c->cfg.discardConsumed;
   // direct mode on an edge iff both ends live in this process (raw device
   // pointers of the peer's buffers are valid here); both ends compute the same
-  p.directNext = c->cfg.directMode && !c->nextIpc;
-  p.directPrev = c->cfg.directMode && !c->prevIpc;
+  p.directNext = rd.directNext;
+  p.directPrev = rd.directPrev;
   p.rings = c->ringsDev;
   p.llLocal = c->arena + c->dataBytes + c->flagsBytes;
   p.llSliceBytes = c->cfg.llSliceBytes;
@@ -741,6 +770,7 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   p.directRead = c->cfg.directRead && c->cfg.directMode;
   p.blocksPerSM = c->cfg.blocksPerSM;
   p.l2Hints = c->cfg.l2Hints;
+  p.stallNs = c->cfg.stallNs;
   Launcher* L = new Launcher();
   if ((r = launcher_start(L, {c})) != occlSuccess) {
     launcher_stop(L);
@@ -781,7 +811,7 @@ occlResult_t occlCommSplit(occlComm_t parent, int nmembers, const int* members, 
   if (!parent || !members || !out || nmembers < 1) return occlInvalidArgument;
   occlComm* P = parent;
   if (P->parent || !P->connected) return occlInvalidUsage;          // split a root communicator
-  if (P->nrings >= kMaxRings) return occlInvalidUsage;
+  if (P->freeRings.empty() && P->nrings >= kMaxRings) return occlInvalidUsage;
   std::vector<char> seen(P->nranks, 0);
   int me = -1;
   for (int i = 0; i < nmembers; ++i) {
@@ -826,15 +856,19 @@ occlResult_t occlCommSplit(occlComm_t parent, int nmembers, const int* members, 
   rd.flagsPrev = pa + P->handles[pq].flagsOffset;
   rd.nranks = nmembers;
   rd.rank = me;
-  rd.directNext = P->cfg.directMode && !P->peerIpc[nq];
-  rd.directPrev = P->cfg.directMode && !P->peerIpc[pq];
+  rd.directNext = P->cfg.directMode && !P->peerIpc[nq] && !P->cfg.forceSysScope;
+  rd.directPrev = P->cfg.directMode && !P->peerIpc[pq] && !P->cfg.forceSysScope;
   // the new entry is written before any submission names it (the SQE's release
   // store orders it for the daemon)
-  if (cudaMemcpy(P->ringsDev + P->nrings, &rd, sizeof(rd), cudaMemcpyHostToDevice) != cudaSuccess)
+  // a destroyed child's slot is reused: the ids bound to it were retired
+  const int slot = P->freeRings.empty() ? P->nrings : P->freeRings.back();
+  if (cudaMemcpy(P->ringsDev + slot, &rd, sizeof(rd), cudaMemcpyHostToDevice) != cudaSuccess)
     return occlCudaError;
+  if (slot == P->nrings) P->nrings++;
+  else P->freeRings.pop_back();
   occlComm* c = new occlComm();
   c->parent = P;
-  c->sub = P->nrings++;
+  c->sub = slot;
   c->nranks = nmembers;
   c->rank = me;
   c->dev = P->dev;
@@ -869,8 +903,11 @@ occlResult_t occlCommDestroy(occlComm_t c) {
         if (R->owner[id] == c) try_complete(R, id);
       if (c->inflight.load() > 0) return occlInvalidUsage;
     }
-    for (int id = 0; id < R->cfg.maxColl; ++id)
+    for (int id = 0; id < R->cfg.maxColl; ++id) {
       if (R->owner[id] == c) R->owner[id] = nullptr;
+      if (R->boundSub[id] == c->sub) R->boundSub[id] = -2;   // retired: its counters belong to that ring
+    }
+    R->freeRings.push_back(c->sub);
     R->children--;
     delete c;
     return occlSuccess;
@@ -888,12 +925,19 @@ occlResult_t occlCommDestroy(occlComm_t c) {
     {
       std::lock_guard<std::mutex> lk(L->mu);
       if (daemon_running(L)) {
-        // Exiting SQE to every member: the daemon drains and exits
+        // Exiting SQE to every member: the daemon drains and exits.
+        // Each waits for a free SQ slot as push_sqe does (a running daemon always
+        // drains the SQ, invariant I4); a daemon that stopped needs no Exiting SQE.
         for (occlComm* m : L->members) {
           Sqe e{};
           e.kind = kExit;
           std::lock_guard<std::mutex> g(m->sqMu);
-          write_sqe(m, e);
+          bool room = true;
+          while (m->sqTail.load() - min_cursor(m) >= (uint64_t)m->cfg.sqDepth) {
+            if (!daemon_running(L)) { room = false; break; }
+            std::this_thread::yield();
+          }
+          if (room) write_sqe(m, e);
         }
       }
     }
@@ -941,9 +985,9 @@ occlResult_t occlTest(occlComm_t c, int id, int* done) {
   c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c || !done || id < 0) return occlInvalidArgument;
   if (id >= c->cfg.maxColl) return occlRegistryFull;
-  if (c->subSeq[id] == 0) return occlUnknownId;
-  if (c->state[id].load() == 1) try_complete(c, id);
-  *done = c->state[id].load() == 0;
+  if (tok_seq(c->tok[id].load()) == 0) return occlUnknownId;
+  if (tok_inflight(c->tok[id].load())) try_complete(c, id);
+  *done = !tok_inflight(c->tok[id].load());
   if (!*done && comm_sticky(c)) return occlCudaError;
   return occlSuccess;
 }
@@ -952,13 +996,13 @@ occlResult_t occlWait(occlComm_t c, int id, int64_t timeoutNs) {
   c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c || id < 0) return occlInvalidArgument;
   if (id >= c->cfg.maxColl) return occlRegistryFull;
-  if (c->subSeq[id] == 0) return occlUnknownId;
+  if (tok_seq(c->tok[id].load()) == 0) return occlUnknownId;
   const uint64_t t0 = now_ns();
   uint64_t it = 0;
   for (;;) {
-    if (c->state[id].load(std::memory_order_acquire) == 0) return occlSuccess;
+    if (!tok_inflight(c->tok[id].load(std::memory_order_acquire))) return occlSuccess;
     if (try_complete(c, id)) return occlSuccess;
-    if (c->state[id].load() == 0) return occlSuccess;
+    if (!tok_inflight(c->tok[id].load())) return occlSuccess;
     if (comm_sticky(c)) return occlCudaError;
     if ((++it & 1023) == 0) {
       if (c->L) {
@@ -977,7 +1021,7 @@ occlResult_t occlSetCallback(occlComm_t c, int id, occlCallback_t cb, void* arg)
   c = root_of(c);                                      // sub-communicators use their root's daemon
   if (!c || id < 0) return occlInvalidArgument;
   if (id >= c->cfg.maxColl) return occlRegistryFull;
-  if (c->state[id].load() == 1) return occlInvalidUsage;   // rebinding only between submissions
+  if (tok_inflight(c->tok[id].load())) return occlInvalidUsage;   // rebinding only between submissions
   c->cbArg[id] = arg;
   c->cb[id] = cb;
   return occlSuccess;

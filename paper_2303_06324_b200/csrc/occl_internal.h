@@ -179,6 +179,9 @@ struct DaemonParams {
   int directRead;                   // 1: the first reduce step reads a same-process upstream's send buffer
   int blocksPerSM;                  // 1 or 2 co-resident daemon blocks per SM
   int l2Hints;                      // evict-first L2 policy for user-buffer loads / stores
+  uint32_t* quitWord;               // device, per launch: quit votes | latch (zeroed before each launch)
+  uint32_t quitTotal;               // blocks of the launch (G x fused members)
+  uint64_t stallNs;                 // FIFO: all entries stuck when none progressed for this long (0: off)
 };
 
 }  // namespace occl

@@ -9,6 +9,7 @@
 """
 from __future__ import annotations
 
+import threading
 import time
 
 import torch
@@ -112,3 +113,71 @@ def host_latency(comms, job, reps=20, timeout_s=60.0):
 def busbw_factor(kind, n):
     return {"allreduce": 2 * (n - 1) / n, "allgather": (n - 1) / n, "reducescatter": (n - 1) / n,
             "broadcast": 1.0}[kind]
+
+
+def live_run(comms, jobs, orders, delays, iterations=1, timeout_s=300.0, orders_fn=None, delays_fn=None):
+    """Asynchronous arrival into a LIVE daemon.
+
+    One submitter thread per local rank.  After a common barrier each thread
+    walks its own order, sleeping delays[local][k] before its k-th submission,
+    then waits for all of its collectives; with iterations > 1 it repeats
+    (ids are resubmitted after local completion, like DP buckets every step).
+    The daemon runs event-driven (autoLaunch = 1): it is (re)launched by the
+    host supervisor on new SQEs and may quit voluntarily when idle.
+
+    jobs[k] = (coll_id, kind, dtype, count, root, bufs) with bufs[local] = (send, recv).
+    orders_fn(it) / delays_fn(it) override orders / delays per iteration.
+    Returns {"makespan_ms", "iter_ms": [...], "submit_ms": per-rank submission
+    span}; host CLOCK_MONOTONIC (one box, one process)."""
+    n = len(comms)
+    dev = comms[0].dev
+    torch.cuda.current_stream(dev).synchronize()
+    for c in comms:
+        c.set_auto_launch(True)
+    bar = threading.Barrier(n + 1)
+    first = [[None] * iterations for _ in range(n)]
+    last = [[None] * iterations for _ in range(n)]
+    errors = []
+
+    def worker(li):
+        c = comms[li]
+        try:
+            bar.wait()
+            for it in range(iterations):
+                od = orders_fn(it)[li] if orders_fn else orders[li]
+                dl = delays_fn(it)[li] if delays_fn else delays[li]
+                t_next = time.perf_counter()
+                for pos, k in enumerate(od):
+                    t_next += dl[pos]
+                    dt = t_next - time.perf_counter()
+                    if dt > 0:
+                        time.sleep(dt)
+                    cid, kind, dtype, count, root, bufs = jobs[k]
+                    s, r = bufs[li]
+                    if first[li][it] is None:
+                        first[li][it] = time.perf_counter()
+                    c.submit(kind, s, r, cid, count, dtype, root)
+                for k in od:
+                    c.wait(jobs[k][0], timeout_s)
+                last[li][it] = time.perf_counter()
+        except Exception as e:  # noqa: BLE001 -- surfaced by the caller
+            errors.append((li, e))
+            bar.abort()
+
+    ts = [threading.Thread(target=worker, args=(li,), daemon=True) for li in range(n)]
+    for t in ts:
+        t.start()
+    try:
+        bar.wait()
+    except threading.BrokenBarrierError:
+        pass
+    for t in ts:
+        t.join(timeout_s * max(1, iterations))
+    if errors:
+        raise errors[0][1]
+    if any(t.is_alive() for t in ts):
+        raise TimeoutError("live_run: submitter threads did not finish")
+    iter_ms = [(max(last[r][it] for r in range(n)) - min(first[r][it] for r in range(n))) * 1e3
+               for it in range(iterations)]
+    makespan = (max(last[r][-1] for r in range(n)) - min(first[r][0] for r in range(n))) * 1e3
+    return {"makespan_ms": makespan, "iter_ms": iter_ms}

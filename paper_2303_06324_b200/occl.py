@@ -54,7 +54,8 @@ class occlConfig_t(C.Structure):
         ("pipeDepth", C.c_int), ("prefetchSlices", C.c_int), ("discardConsumed", C.c_int), ("l2Hints", C.c_int),
         ("directMode", C.c_int), ("stagingTiles", C.c_int), ("blocksPerSM", C.c_int), ("traceCap", C.c_uint32),
         ("llSliceBytes", C.c_uint32), ("llMaxBytes", C.c_uint32), ("spinNs", C.c_uint32),
-        ("bulkStores", C.c_int), ("directRead", C.c_int),
+        ("bulkStores", C.c_int), ("directRead", C.c_int), ("stallNs", C.c_uint64),
+        ("forceSysScope", C.c_int),
     ]
 
 
@@ -415,19 +416,48 @@ def local_group(nranks, device=0, cfg=None, fuse=True, **overrides):
     return comms
 
 
+def occlCommInit(nranks, rank, dev, allgather, cfg=None):
+    """occlCommInit with a Python bootstrap all-gather: ``allgather(mine: bytes)
+    -> list[bytes]`` (rank-major) is called once, from inside the C call."""
+    failure = []
+
+    def ag(inp, out, nbytes, ctx):
+        try:
+            parts = allgather(C.string_at(inp, nbytes))
+            blob = b"".join(bytes(p).ljust(nbytes, b"\0")[:nbytes] for p in parts)
+            if len(blob) != nbytes * nranks:
+                return 1
+            C.memmove(out, blob, len(blob))
+            return 0
+        except Exception as e:  # noqa: BLE001 -- reported after the C call returns
+            failure.append(e)
+            return 1
+
+    cb = ALLGATHER(ag)
+    h = C.c_void_p()
+    code = _lib().occlCommInit(C.byref(h), nranks, rank, dev, cb, None, C.byref(cfg) if cfg is not None else None)
+    if failure:
+        raise failure[0]
+    check(code, "occlCommInit")
+    return h
+
+
 def process_group(pg=None, device=None, cfg=None, **overrides):
-    """One rank per process over torch.distributed: handles are exchanged with
-    all_gather_object; connectors are opened through CUDA IPC / peer access."""
+    """One rank per process over torch.distributed: occlCommInit with
+    dist.all_gather_object as the bootstrap all-gather; connectors are opened
+    through CUDA IPC / peer access."""
     import torch
     import torch.distributed as dist
     rank, n = dist.get_rank(pg), dist.get_world_size(pg)
     device = torch.cuda.current_device() if device is None else device
     cfg = cfg if cfg is not None else occlConfigDefault(**overrides)
-    h = occlCommCreate(n, rank, device, cfg)
-    mine = occlCommGetHandle(h)
-    allh = [None] * n
-    dist.all_gather_object(allh, mine, group=pg)
-    occlCommConnect(h, allh)
+
+    def allgather(mine):
+        allh = [None] * n
+        dist.all_gather_object(allh, mine, group=pg)
+        return allh
+
+    h = occlCommInit(n, rank, device, allgather, cfg)
     return Comm(h, n, rank, device, cfg)
 
 

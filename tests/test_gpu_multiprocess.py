@@ -33,11 +33,15 @@ def test_bench_multiprocess_path():
     env = dict(os.environ, OCCL_BENCH_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"), "--gpus", "2",
-           "--ranks", "8", "--size-mib", "8", "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu", "--check"]
+           "--size-mib", "8", "--sizes", "2,8", "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu", "--check"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=400, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]
     d = lines[0]
-    assert d["n_gpus"] == 2 and d["value"] > 0 and d["check"]["bit_exact"]
-    assert d["config"]["ranks_per_gpu"] == 4
+    # one rank per process (the metric's N-GPU configuration), occlCommInit over torch.distributed
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["ranks_per_gpu"] == 1
+    head = [r for r in d["sweep"] if r["size_bytes"] == 8 << 20][0]
+    assert head["check"]["bit_exact"] and len(d["sweep"]) == 2
+    assert d["roofline"]["bound"] == "nvlink" and d["scaling"] == "weak"
+    assert "unavailable" in d["baseline"]["nccl"]                 # gloo plumbing on one GPU: no NCCL arm

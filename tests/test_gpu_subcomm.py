@@ -96,3 +96,43 @@ def test_split_errors_and_lifetime(occl_mod):
             k.destroy()
     finally:
         occl_mod.destroy_group(comms)
+
+
+def test_collid_bound_to_first_ring_and_slot_reuse(occl_mod):
+    """a collId's connector counters belong to the ring of its
+    first submission, so submitting it on another rank set is refused
+    (occlInvalidUsage) instead of pairing counters of different edges; a
+    destroyed child retires its ids.  Ring slots of destroyed children are
+    reused: 40 split / destroy cycles (> 31 slots) all work."""
+    comms = occl_mod.local_group(4, 0, **CFG)
+    try:
+        x = [torch.full((4096,), float(q + 1), device=0) for q in range(4)]
+        torch.cuda.synchronize()
+        kids = [comms[q].split([0, 1]) for q in (0, 1)]
+        for k, t in zip(kids, x):
+            k.all_reduce(t, t, 6)
+        for k in kids:
+            k.wait(6, U.WAIT_S)
+        assert torch.all(x[0] == 3.0)
+        with pytest.raises(occl_mod.OcclError) as e:
+            comms[0].all_reduce(x[2], x[2], 6)               # id 6 is bound to the {0, 1} ring
+        assert e.value.code == occl_mod.occlInvalidUsage
+        for k in kids:
+            k.destroy()
+        with pytest.raises(occl_mod.OcclError) as e:
+            comms[0].all_reduce(x[2], x[2], 6)               # retired with its ring
+        assert e.value.code == occl_mod.occlInvalidUsage
+        for cycle in range(40):
+            pair = [cycle % 4, (cycle + 1) % 4]
+            ks = [comms[q].split(pair) for q in pair]
+            y = [torch.full((1000,), float(cycle + i), device=0) for i in range(2)]
+            torch.cuda.synchronize()
+            for k, t in zip(ks, y):
+                k.all_reduce(t, t, 8 + cycle)                 # fresh id per ring
+            for k in ks:
+                k.wait(8 + cycle, U.WAIT_S)
+            assert torch.all(y[0] == float(2 * cycle + 1))
+            for k in ks:
+                k.destroy()
+    finally:
+        occl_mod.destroy_group(comms)

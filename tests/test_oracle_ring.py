@@ -461,3 +461,68 @@ def test_o1_equals_o2_execution_64bit(op, dtype):
         for r in range(n):
             if exp[r] is not None:
                 assert np.array_equal(_bits(sim.results[(r, 0, 0)]), _bits(exp[r])), (kind, r)
+
+
+# ----------------------------------------------------------------------------- R24: signed zeros, specials
+def test_ieee_max_min_signed_zero_closed_form():
+    """IEEE 754-2019 maximum / minimum (reading R24): -0 < +0, in either operand
+    order (numpy's np.maximum returns its FIRST operand on a tie, so it is not
+    the definition)."""
+    pz, nz = np.float32(0.0), np.float32(-0.0)
+    for a, b in ((pz, nz), (nz, pz)):
+        assert not np.signbit(ring.ieee_max(a, b)) and ring.ieee_max(a, b) == 0
+        assert np.signbit(ring.ieee_min(a, b)) and ring.ieee_min(a, b) == 0
+    assert np.signbit(ring.ieee_max(nz, nz)) and not np.signbit(ring.ieee_min(pz, pz))
+    inf = np.float32(np.inf)
+    assert ring.ieee_max(-inf, nz) == 0 and np.signbit(ring.ieee_max(-inf, nz))
+    assert ring.ieee_min(inf, -inf) == -inf
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
+@pytest.mark.parametrize("n", [2, 3, 8])
+def test_signed_zero_folds_are_order_free(dtype, n):
+    """Every ring order gives the same max / min of signed zeros: +0 iff some rank
+    holds +0 (max), -0 iff some rank holds -0 (min) -- checked against that
+    closed form for all 2^n sign patterns; and a sum of zeros is -0 iff every
+    operand is -0 (round to nearest, IEEE 754 §6.3)."""
+    pats = np.array([[(m >> r) & 1 for r in range(n)] for m in range(1 << n)], dtype=bool)   # True = -0
+    if dtype == "f32":
+        mk = lambda neg: np.where(neg, np.float32(-0.0), np.float32(0.0)).astype(np.float32)
+        sign = np.signbit
+    elif dtype == "f16":
+        mk = lambda neg: np.where(neg, np.float16(-0.0), np.float16(0.0)).astype(np.float16)
+        sign = np.signbit
+    else:
+        mk = lambda neg: np.where(neg, np.uint16(0x8000), np.uint16(0)).astype(np.uint16)
+        sign = lambda v: (np.asarray(v) & 0x8000) != 0
+    xs = [mk(pats[:, r]) for r in range(n)]
+    assert np.array_equal(sign(ring.allreduce(xs, dtype, "max")), pats.all(axis=1))
+    assert np.array_equal(sign(ring.allreduce(xs, dtype, "min")), pats.any(axis=1))
+    assert np.array_equal(sign(ring.allreduce(xs, dtype, "sum")), pats.all(axis=1))
+
+
+def test_special_generator_covers_every_category():
+    from inputs import special
+    for dtype, (tot, eb, mb) in special.FORMATS.items():
+        b = special.special_bits(dtype, 1, 0, 200_000).astype(np.uint64)
+        e = (b >> np.uint64(mb)) & np.uint64((1 << eb) - 1)
+        m = b & np.uint64((1 << mb) - 1)
+        s = b >> np.uint64(tot - 1)
+        top = np.uint64((1 << eb) - 1)
+        assert ((e == 0) & (m == 0) & (s == 0)).any() and ((e == 0) & (m == 0) & (s == 1)).any()   # +0, -0
+        assert ((e == 0) & (m != 0)).any()                                                     # subnormal
+        assert ((e == top) & (m == 0) & (s == 0)).any() and ((e == top) & (m == 0) & (s == 1)).any()   # +-Inf
+        assert not ((e == top) & (m != 0)).any()                                              # no NaN input
+        assert np.array_equal(b, special.special_bits(dtype, 1, 0, 200_000).astype(np.uint64))  # seeded
+
+
+def test_subnormal_sums_are_exact_gradual_underflow():
+    """Two f32 subnormals add exactly (their sum has at most 25 significant bits
+    at the subnormal exponent, so it is representable or overflows into the
+    normal range exactly): the oracle does not flush to zero."""
+    a = np.array([1, 0x007FFFFF, 0x00400000], dtype=np.uint32).view(np.float32)
+    b = np.array([1, 1, 0x00400000], dtype=np.uint32).view(np.float32)
+    got = ring.add(a, b, "f32").view(np.uint32)
+    assert got.tolist() == [2, 0x00800000, 0x00800000]
+    # bf16: subnormal 0x0001 + 0x0001 = 0x0002 (exact), through the f32 widening
+    assert ring.add(np.array([1], np.uint16), np.array([1], np.uint16), "bf16").tolist() == [2]
