@@ -607,43 +607,52 @@ __device__ __noinline__ bool sq_fetch(const DaemonParams& p, const Smem& m, int 
     st_relaxed(p.mirrorTail + 2, m, 0);
   }
   const uint64_t t0 = t;
-  constexpr int B = 8;
+  constexpr int B = 4;
   for (;;) {
-    // one PCIe round trip: the sequence numbers of up to B slots, read in parallel
+    // ONE PCIe round trip: all chunks of up to B slots, read in parallel.  Every
+    // 16-B chunk carries the SQE's stamp (SqeWire), so a slot is valid iff its
+    // five stamps match -- no acquire-then-payload second trip is needed
     uint64_t room = p.sqDepth - (t - minCur);
     if (room > 256 - (t - t0)) room = 256 - (t - t0);
     const int nb = room < (uint64_t)B ? (int)room : B;   // (at most 256 SQEs per call)
     if (nb <= 0) break;
-    uint64_t seqs[B];
+    uint4 w[B][kWireChunks];
 #pragma unroll
-    for (int i = 0; i < B; ++i)
-      if (i < nb) seqs[i] = ld_relaxed(&p.sq[(t + i) % p.sqDepth].seq, 1);
+    for (int i = 0; i < B; ++i) {
+      if (i < nb) {
+        const SqeWire* s = p.sq + (t + i) % p.sqDepth;
+#pragma unroll
+        for (int q = 0; q < kWireChunks; ++q)
+          asm volatile("ld.relaxed.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(w[i][q].x), "=r"(w[i][q].y), "=r"(w[i][q].z), "=r"(w[i][q].w) : "l"(s->c[q])
+                       : "memory");
+      }
+    }
     int valid = 0;
 #pragma unroll
-    for (int i = 0; i < B; ++i)
-      if (valid == i && i < nb && seqs[i] == t + i + 1) valid = i + 1;   // seq is written last by the host
+    for (int i = 0; i < B; ++i) {
+      bool ok = valid == i && i < nb;
+      const uint32_t stamp = (uint32_t)(t + i + 1);
+#pragma unroll
+      for (int q = 0; q < kWireChunks; ++q) ok = ok && w[i][q].x == stamp;
+      if (ok) valid = i + 1;
+    }
     trace_at(p, *m.tr, b, kEvMark, valid, 2);
     if (!valid) break;
-    fence_sys();                                               // acquire: the payload loads come after
-    trace_at(p, *m.tr, b, kEvMark, valid, 3);
-    // a second round trip: every valid SQE's payload (4 independent 16-B loads each)
-    uint4 w[B][4];
 #pragma unroll
     for (int i = 0; i < B; ++i) {
       if (i >= valid) break;
-      const char* base = reinterpret_cast<const char*>(p.sq + (t + i) % p.sqDepth);
+      uint32_t words[15];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        asm volatile("ld.relaxed.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(w[i][q].x), "=r"(w[i][q].y), "=r"(w[i][q].z), "=r"(w[i][q].w) : "l"(base + 16 * q)
-                     : "memory");
-    }
-#pragma unroll
-    for (int i = 0; i < B; ++i) {
-      if (i >= valid) break;
+      for (int q = 0; q < kWireChunks; ++q) {
+        words[3 * q] = w[i][q].y; words[3 * q + 1] = w[i][q].z; words[3 * q + 2] = w[i][q].w;
+      }
+      Sqe e;
+      sqe_from_words(words, t + i + 1, e);
+      const uint4* src = reinterpret_cast<const uint4*>(&e);
       uint4* dst = reinterpret_cast<uint4*>(p.sqMirror + (t + i) % p.sqDepth);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) st_cg_v4(dst + q, w[i][q]);
+      for (int q = 0; q < 4; ++q) st_cg_v4(dst + q, src[q]);
     }
     t += valid;
     trace_at(p, *m.tr, b, kEvMark, valid, 4);

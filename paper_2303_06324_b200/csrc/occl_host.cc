@@ -14,6 +14,7 @@
 //   * connectors of the ring neighbours are mapped through CUDA IPC (other
 //     processes) or used directly (same process), with peer access enabled.
 #include <cuda_runtime.h>
+#include <emmintrin.h>
 #include <unistd.h>
 
 #include <atomic>
@@ -119,8 +120,8 @@ struct occlComm {
   TraceRec* trace = nullptr;
   uint32_t* traceCount = nullptr;
   // pinned + mapped host memory
-  Sqe* sqHost = nullptr;
-  Sqe* sqDev = nullptr;
+  SqeWire* sqHost = nullptr;
+  SqeWire* sqDev = nullptr;
   uint64_t* sqCurHost = nullptr;
   uint64_t* sqCurDev = nullptr;
   uint64_t* cqHost = nullptr;
@@ -380,10 +381,16 @@ int coll_blocks(const occlComm* c, int kind, size_t count, int dtype) {
 
 void write_sqe(occlComm* c, Sqe& e) {
   const uint64_t t = c->sqTail.load();
-  Sqe* s = &c->sqHost[t % c->cfg.sqDepth];
-  std::memcpy(reinterpret_cast<char*>(s) + 8, reinterpret_cast<const char*>(&e) + 8, sizeof(Sqe) - 8);
+  SqeWire* s = &c->sqHost[t % c->cfg.sqDepth];
+  uint32_t w[15];
+  sqe_to_words(e, w);
+  const uint32_t stamp = (uint32_t)(t + 1);
+  // one aligned 16-B store per chunk: the device sees each chunk old or new
+  for (int k = 0; k < kWireChunks; ++k) {
+    const __m128i v = _mm_set_epi32((int)w[3 * k + 2], (int)w[3 * k + 1], (int)w[3 * k], (int)stamp);
+    _mm_store_si128(reinterpret_cast<__m128i*>(s->c[k]), v);
+  }
   std::atomic_thread_fence(std::memory_order_release);
-  reinterpret_cast<std::atomic<uint64_t>*>(&s->seq)->store(t + 1, std::memory_order_release);
   c->sqTail.store(t + 1);
 }
 
@@ -601,8 +608,8 @@ occlResult_t occlCommCreate(occlComm_t* out, int nranks, int rank, int cudaDev, 
   if ((e = cudaMalloc(&cp->traceCount, G * sizeof(uint32_t))) != cudaSuccess) return fail(e);
   if ((e = cudaMemset(cp->traceCount, 0, G * sizeof(uint32_t))) != cudaSuccess) return fail(e);
   const unsigned flags = cudaHostAllocMapped | cudaHostAllocPortable;
-  if ((e = cudaHostAlloc(&cp->sqHost, cfg.sqDepth * sizeof(Sqe), flags)) != cudaSuccess) return fail(e);
-  std::memset(cp->sqHost, 0, cfg.sqDepth * sizeof(Sqe));
+  if ((e = cudaHostAlloc(&cp->sqHost, cfg.sqDepth * sizeof(SqeWire), flags)) != cudaSuccess) return fail(e);
+  std::memset(cp->sqHost, 0, cfg.sqDepth * sizeof(SqeWire));
   if ((e = cudaHostGetDevicePointer(&cp->sqDev, cp->sqHost, 0)) != cudaSuccess) return fail(e);
   if ((e = cudaHostAlloc(&cp->sqCurHost, G * sizeof(uint64_t), flags)) != cudaSuccess) return fail(e);
   std::memset(cp->sqCurHost, 0, G * sizeof(uint64_t));
@@ -1161,7 +1168,7 @@ occlResult_t occlGetFootprint(occlComm_t c, occlFootprint_t* out) {
                (size_t)G * c->cfg.traceCap * sizeof(TraceRec) + G * sizeof(uint32_t) +
                (c->ringsDev ? kMaxRings * sizeof(RingDesc) : 0);
   out->device = out->connectorData + out->connectorFlags + out->llLines + out->contexts + out->other;
-  out->pinnedHost = c->cfg.sqDepth * sizeof(Sqe) + G * sizeof(uint64_t) + M * sizeof(uint64_t);
+  out->pinnedHost = c->cfg.sqDepth * sizeof(SqeWire) + G * sizeof(uint64_t) + M * sizeof(uint64_t);
   out->perBlockPerColl = (double)(out->device) / (double)(M * G);
   return occlSuccess;
 }

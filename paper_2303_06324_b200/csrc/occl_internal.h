@@ -38,6 +38,51 @@ struct alignas(64) Sqe {
 };
 static_assert(sizeof(Sqe) == 64, "Sqe must be 64 B");
 
+// The SQE as it sits in the pinned host SQ: five 16-B chunks, each stamped with
+// the low 32 bits of the SQE's 1-based sequence number.  The host writes every
+// chunk with ONE aligned 16-B store, so a device read of a chunk sees either
+// the old or the new chunk, never a mix; a slot is valid iff all five stamps
+// equal the expected sequence number.  The daemon thus reads an SQE in a single
+// PCIe round trip -- no "seq first, payload after an acquire" second trip.
+constexpr int kWireChunks = 5;
+struct alignas(128) SqeWire {
+  uint32_t c[8][4];    // chunk k = {stamp, w0, w1, w2}; chunks 5..7 unused (128-B slot stride)
+};
+static_assert(sizeof(SqeWire) == 128, "SqeWire must be 128 B");
+// Payload words of an Sqe in chunk order (15 x 32 bit; seq travels as the stamp).
+#if defined(__CUDACC__)
+#define OCCL_HD __host__ __device__ __forceinline__
+#else
+#define OCCL_HD inline
+#endif
+OCCL_HD void sqe_to_words(const Sqe& e, uint32_t w[15]) {
+  w[0] = e.collId;
+  w[1] = (uint32_t)e.kind | ((uint32_t)e.dtype << 16);
+  w[2] = (uint32_t)e.op | ((uint32_t)e.nblocks << 16);
+  w[3] = (uint32_t)e.subSeq; w[4] = (uint32_t)(e.subSeq >> 32);
+  w[5] = (uint32_t)e.root;
+  w[6] = (uint32_t)e.count; w[7] = (uint32_t)(e.count >> 32);
+  w[8] = (uint32_t)e.priority;
+  w[9] = (uint32_t)e.sendbuff; w[10] = (uint32_t)(e.sendbuff >> 32);
+  w[11] = (uint32_t)e.sub;
+  w[12] = (uint32_t)e.recvbuff; w[13] = (uint32_t)(e.recvbuff >> 32);
+  w[14] = 0;
+}
+OCCL_HD void sqe_from_words(const uint32_t w[15], uint64_t seq, Sqe& e) {
+  e.seq = seq;
+  e.collId = w[0];
+  e.kind = (uint16_t)w[1]; e.dtype = (uint16_t)(w[1] >> 16);
+  e.op = (uint16_t)w[2]; e.nblocks = (uint16_t)(w[2] >> 16);
+  e.subSeq = (uint64_t)w[3] | ((uint64_t)w[4] << 32);
+  e.root = (int32_t)w[5];
+  e.count = (uint64_t)w[6] | ((uint64_t)w[7] << 32);
+  e.priority = (int32_t)w[8];
+  e.sendbuff = (uint64_t)w[9] | ((uint64_t)w[10] << 32);
+  e.sub = (uint16_t)w[11];
+  e.pad = 0;
+  e.recvbuff = (uint64_t)w[12] | ((uint64_t)w[13] << 32);
+}
+
 constexpr int kMaxRings = 32;           // communicator + sub-communicators served by one daemon
 // One ring the daemon serves (the static context carries the
 // collective's own nranks / rank).  Connectors and flags of a collective live at
@@ -134,7 +179,7 @@ struct alignas(16) TraceRec {
 };
 
 struct DaemonParams {
-  const Sqe* sq;                    // mapped host SQ
+  const SqeWire* sq;                // mapped host SQ (stamped wire format)
   volatile uint64_t* sqCursorHost;  // mapped host [G]: [0] = SQEs copied to the mirror (slots below are free)
   Sqe* sqMirror;                    // device [sqDepth]: copy of the host SQ read by every block
   uint64_t* mirrorTail;             // device: [0] SQEs in the mirror, [1] fetch lock, [2] cached min block cursor

@@ -80,6 +80,12 @@ def main():
     ap.add_argument("--grid", type=int, default=18)
     ap.add_argument("--spin-ns", type=int, default=0)
     ap.add_argument("--stall-ns", type=int, default=-1)
+    ap.add_argument("--spin-base", type=int, default=0)
+    ap.add_argument("--spin-step", type=int, default=-1)
+    ap.add_argument("--spin-min", type=int, default=0)
+    ap.add_argument("--spin-cap", type=int, default=0)
+    ap.add_argument("--quit-idle-ns", type=int, default=0)
+    ap.add_argument("--tag", default="")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     n = args.ranks
@@ -92,6 +98,12 @@ def main():
             extra = {"spinNs": args.spin_ns} if args.spin_ns else {}
             if args.stall_ns >= 0:
                 extra["stallNs"] = args.stall_ns
+            for k, v in (("spinBase", args.spin_base), ("spinMin", args.spin_min), ("spinCap", args.spin_cap),
+                         ("quitIdleNs", args.quit_idle_ns)):
+                if v:
+                    extra[k] = v
+            if args.spin_step >= 0:
+                extra["spinStep"] = args.spin_step
             comms = harness.ring(n, 0, gridBlocks=args.grid, maxColl=256, orderPolicy=policy, stickiness=stick,
                                  **extra)
             fifo = policy == 0
@@ -109,7 +121,7 @@ def main():
                 for rep in range(args.repeats):
                     tc, sc, _ = one(comms, jobs, n, ncoll, iters, seed, rep, mean_gap, "consistent")
                     tr, sr, rr = one(comms, jobs, n, ncoll, iters, seed, rep, mean_gap, "random")
-                    row = {"workload": wname, "variant": vname, "seed": seed, "repeat": rep, "ranks": n,
+                    row = {"tag": args.tag, "knobs": extra, "workload": wname, "variant": vname, "seed": seed, "repeat": rep, "ranks": n,
                            "ncoll": ncoll, "iterations": iters, "mean_gap_us": mean_gap * 1e6,
                            "ms_consistent": tc, "ms_random": tr, "overhead": tr / tc - 1.0,
                            "preempt_consistent": sc["preemptions"], "preempt_random": sr["preemptions"],
@@ -131,7 +143,7 @@ def main():
             if not rs:
                 continue
             ov = sorted(r["overhead"] for r in rs)
-            summ.append({"workload": wname, "variant": vname, "runs": len(rs),
+            summ.append({"tag": args.tag, "workload": wname, "variant": vname, "runs": len(rs),
                          "ms_consistent_median": statistics.median(r["ms_consistent"] for r in rs),
                          "ms_random_median": statistics.median(r["ms_random"] for r in rs),
                          "overhead_median": statistics.median(ov), "overhead_min": ov[0], "overhead_max": ov[-1],
