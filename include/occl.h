@@ -106,7 +106,8 @@ typedef struct {
   int pipeDepth;          /* slices in flight between the control warp and the data warps (1..8)   */
   int prefetchSlices;     /* send-buffer slices prefetched into L2 ahead of the issue cursor      */
   int discardConsumed;    /* 1 = drop consumed connector lines from L2 without write-back         */
-  int l2Hints;            /* 1 = evict-first L2 policy for send/recv-buffer streams; 2 = also evict-last for connector stores */
+  int l2Hints;            /* 1 = evict-first L2 policy for send/recv-buffer streams; 2 = also evict-last for connector stores;
+                             3 = also evict-last for direct sends the downstream forwards (demoted once read) */
   int directMode;         /* 1 = final data goes straight into a same-process peer's recv buffer  */
   int stagingTiles;       /* TMA staging ring depth per block (1..6), 32 KiB of shared memory each */
   int blocksPerSM;        /* 1 (up to 608 threads) or 2 (up to 384 threads, <= 3 staging tiles)    */
@@ -121,6 +122,8 @@ typedef struct {
   int forceSysScope;      /* 1 = treat every peer as another process (CUDA IPC): system-scope fences,
                              connector-only edges (no direct mode / direct read) -- the one-process-per-GPU
                              data path, selectable on one device for testing and benchmarking */
+  int cqMode;             /* CQ variant: 0 = one slot per collId (default), 1 = vanilla
+                             MPSC ring (entry, fence, in-order tail), 2 = packed 64-bit {stamp, id} ring */
 } occlConfig_t;
 
 /* Aggregate counters (device counters summed over blocks/collectives). */
@@ -158,6 +161,8 @@ typedef struct {
   uint64_t nCtxLoad;
   uint64_t cycCtxSave;    /* lazy dynamic-context saves              */
   uint64_t nCtxSave;
+  uint64_t cycCqe;        /* CQE writes: completing increment -> host store issued (cfg.cqMode) */
+  uint64_t nCqe;
 } occlProbes_t;
 
 /* One device trace record (%globaltimer ns).  tag = event << 24 | collId; for

@@ -3,6 +3,7 @@ to the GPU box with the repo snapshot).
 
   lib/libocclb200.so : the product -- daemon kernel + host runtime behind include/occl.h
   lib/libocclgen.so  : test/bench support -- the seeded input generator on the GPU
+  lib/libocclbench.so: bench support -- native per-rank latency harness over the C-ABI
 """
 from __future__ import annotations
 
@@ -22,7 +23,9 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shar
 TARGETS = {
     "libocclb200.so": ["occl_daemon.cu", "occl_host.cc"],
     "libocclgen.so": ["testgen.cu"],
+    "libocclbench.so": ["bench_native.cc"],     # bench / test harness over the C-ABI (links the product)
 }
+LINK = {"libocclbench.so": ["-L" + LIB, "-locclb200", "-Xlinker", "-rpath=$ORIGIN"]}
 
 
 def _stale(out, srcs):
@@ -41,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> list[str]:
         out = os.path.join(LIB, name)
         if not force and not _stale(out, srcs):
             continue
-        cmd = [NVCC] + COMMON + [os.path.join(CSRC, s) for s in srcs] + ["-o", out + ".tmp"]
+        cmd = [NVCC] + COMMON + [os.path.join(CSRC, s) for s in srcs] + LINK.get(name, []) + ["-o", out + ".tmp"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

@@ -202,7 +202,8 @@ enum : int { A_RECV = 1, A_REDUCE = 2, A_COPY = 4, A_SEND = 8,
              A_DIN = 16,    // direct receive: the upstream wrote the data into our recv buffer
              A_DOUT = 32,   // direct send: write into the downstream's recv buffer, not its connector
              A_LL = 64,     // LL protocol: 16-B lines {data, flag, data, flag}, no release fence
-             A_DREAD = 128 }; // direct read: the input is the upstream's send buffer (no message)
+             A_DREAD = 128,   // direct read: the input is the upstream's send buffer (no message)
+             A_KEEPOUT = 256 };  // direct send whose data the downstream re-reads next hop (L2 evict-last)
 enum : int {
   P_SEND = A_SEND,
   P_RECV = A_RECV | A_COPY,
@@ -379,6 +380,17 @@ __device__ __forceinline__ int directify(int prim, int kind, int n, int step, bo
   return prim;
 }
 
+// Does the downstream read (and forward) the data we direct-send at `step`?  Then
+// it is worth keeping in L2 for one hop (l2Hints == 3).
+__device__ __forceinline__ bool downstream_forwards(int kind, int n, int r, int root, int step) {
+  switch (kind) {
+    case kAllReduce: return step + 1 <= 2 * n - 3;
+    case kAllGather: return step + 1 <= n - 2;
+    case kBroadcast: return md(r - root, n) + 1 <= n - 2;
+    default: return false;
+  }
+}
+
 __device__ __forceinline__ int elem_size(int dt) {
   return (dt == kBF16 || dt == kF16) ? 2 : ((dt == kI64 || dt == kF64) ? 8 : 4);
 }
@@ -463,6 +475,7 @@ struct Sched {
   int way;
   unsigned long long cycRun, cycPoll, cycAcqFence, cycRelFence, nCommit;   // probes
   unsigned long long cycCtxLoad, nCtxLoad, cycCtxSave, nCtxSave;
+  unsigned long long cycCqe, nCqe;
 };
 
 // Control -> data warp pipeline: slice descriptors in a ring of `depth` buffers.
@@ -689,9 +702,29 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
       fence_acq_rel(0);                               // gpu scope: the CQE writer's fence.sys is cumulative
       const uint32_t old = atom_add_acq_rel(&p.complCnt[id], 1u);
       if (old + 1 == cx.nblocks) {
+        const long long tq = clock64();
         p.complCnt[id] = 0;
-        fence_sys();
-        st_volatile_u64(&p.cqDone[id], cx.s.subSeq);
+        fence_sys();                                  // the collective's data before its CQE
+        if (p.cqMode == 0) {
+          st_volatile_u64(&p.cqDone[id], cx.s.subSeq);  // id slot, single writer (reading R9)
+        } else {
+          const uint64_t slot = atomicAdd((unsigned long long*)p.cqReserve, 1ull);
+          volatile uint64_t* e = p.cqRing + (slot % p.cqDepth);
+          if (p.cqMode == 2) {
+            // optimized ring: {stamp = slot + 1, id} in ONE 64-bit write; the
+            // poller validates the stamp, so no fence and no tail update
+            st_volatile_u64(e, ((slot + 1) << 32) | (uint32_t)id);
+          } else {
+            // vanilla ring: entry, fence, then the tail -- in slot order, so a
+            // block waits (host-memory reads) for its predecessors' tail update
+            st_volatile_u64(e, (uint64_t)(uint32_t)id);
+            fence_sys();
+            while (ld_acquire_sys((const void*)p.cqTail) != slot) {}
+            asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p.cqTail), "l"(slot + 1) : "memory");
+          }
+        }
+        sh.cycCqe += clock64() - tq;
+        ++sh.nCqe;
         p.blkStats[b].cqes++;
         trace_at(p, *m.tr, b, kEvCqe, id, (uint32_t)cx.s.subSeq);
       }
@@ -916,6 +949,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   const char* directIn = p.flagsLocal + cb * kFlagStride + kDirectOff;   // {peer recvbuff, subSeq}
   const bool dOut = R.directNext != 0 && !ll, dIn = R.directPrev != 0 && !ll;
   const bool dRead = p.directRead != 0;
+  const bool keepOut = p.l2Hints >= 3;
   const char* srcIn = p.flagsLocal + cb * kFlagStride + kDirectOff + 16;  // {upstream sendbuff, subSeq}
   // Read-done acknowledgement of direct read (reduce-scatter).  An RS rank's own
   // completion does not depend on its downstream's progress: when its last
@@ -993,6 +1027,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
       int seg;
       step_prim(kind, n, r, root, di.step, inplace, curPrim, seg);
       curPrim = directify(curPrim, kind, n, di.step, dOut, dIn, dRead);
+      if (keepOut && (curPrim & A_DOUT) && downstream_forwards(kind, n, r, root, di.step)) curPrim |= A_KEEPOUT;
       uint64_t sendOff, recvOff, len;
       seg_geom(kind, n, r, count, segLen, seg, sendOff, recvOff, len);
       uint64_t laneHi = laneLo + part;
@@ -1143,6 +1178,8 @@ __device__ __noinline__ void control_main(const DaemonParams& p, int b, Sched& s
   bst.nCtxLoad += sh.nCtxLoad;
   bst.cycCtxSave += sh.cycCtxSave;
   bst.nCtxSave += sh.nCtxSave;
+  bst.cycCqe += sh.cycCqe;
+  bst.nCqe += sh.nCqe;
   // release the data warps (the pipe is drained after every run)
   pipe.ring[issued % D].prim = P_EXIT;
   mbar_arrive(&pipe.full[issued % D]);
@@ -1199,6 +1236,11 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // upstream's next write into the slot).
 __device__ __forceinline__ void discard_l2_line(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" :: "l"(p) : "memory");
+}
+// Demote a line the upstream stored evict-last (l2Hints == 3) once it is read:
+// the final data stays cached only as long as the next hop needs it.
+__device__ __forceinline__ void demote_l2_line(const void* p) {
+  asm volatile("applypriority.global.L2::evict_normal [%0], 128;" :: "l"(p) : "memory");
 }
 __device__ __forceinline__ uint4 lds_v4(const void* p) {
   uint4 v;
@@ -1267,14 +1309,20 @@ __device__ __noinline__ void producer_main(const DaemonParams& p, Pipe& pipe, St
 }
 
 // Compute warps: reduce / copy the staged tiles into the recv buffer and the
-// downstream connector with 128-bit stores.
+// downstream connector with 128-bit stores.  L2 policies by l2Hints (l2):
+//   own recv buffer (final data, not re-read)     : l2 >= 1 evict-first
+//   downstream connector (read once, then discarded): l2 >= 2 evict-last, so the
+//                                                     streamed user buffers leave L2 first
+//   direct send into the downstream's recv buffer : l2 >= 3 evict-last when the
+//     downstream forwards it at its next hop (A_KEEPOUT; it demotes the lines to
+//     normal once read), evict-first on the last hop
 template <int DT, int OP>
 __device__ __forceinline__ void consume_tile(const int prim, char* dst, char* cout, const Stage& s, int sz, int tid,
-                                             int nt, bool hints, uint64_t pol, bool keep, uint64_t polKeep) {
+                                             int nt, int l2, uint64_t polFirst, uint64_t polLast) {
   const bool reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
-  // l2Hints == 2: connector lines (re-read once by the downstream, then discarded)
-  // are stored evict-last so the streamed user buffers leave L2 before them
-  keep = keep && !(prim & A_DOUT);
+  // 0 plain, 1 evict-first, 2 evict-last
+  const int sendPol = !(prim & A_DOUT) ? (l2 >= 2 ? 2 : 0) : (l2 >= 3 ? ((prim & A_KEEPOUT) ? 2 : 1) : 0);
+  const uint64_t sp = sendPol == 2 ? polLast : polFirst;
   uint4* vd = reinterpret_cast<uint4*>(dst);
   uint4* vo = reinterpret_cast<uint4*>(cout);
   const int nv = sz >> 4;
@@ -1282,11 +1330,11 @@ __device__ __forceinline__ void consume_tile(const int prim, char* dst, char* co
     uint4 v = lds_v4(&s.in[i]);
     if (reduce) v = vop<DT, OP>(v, lds_v4(&s.loc[i]));
     if (copy) {
-      if (hints) st_cg_hint(vd + i, v, pol);
+      if (l2 >= 1) st_cg_hint(vd + i, v, polFirst);
       else __stcg(vd + i, v);
     }
     if (send) {
-      if (keep) st_cg_hint(vo + i, v, polKeep);
+      if (sendPol) st_cg_hint(vo + i, v, sp);
       else __stcg(vo + i, v);
     }
   }
@@ -1408,7 +1456,8 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
   const uint32_t D = (uint32_t)p.pipeDepth, S = (uint32_t)p.stages;
   const bool bulk = p.bulkStores != 0;
   const int lane = ctid & 31;
-  const bool hints = p.l2Hints != 0, discard = p.discardConsumed != 0, keep = p.l2Hints == 2;
+  const bool discard = p.discardConsumed != 0;
+  const int l2 = p.l2Hints;
   const uint64_t pol = policy_evict_first(), polKeep = policy_evict_last();
   const bool leader = ctid == 0;                       // probes
   unsigned long long cWait = 0, cData = 0, nData = 0;
@@ -1450,12 +1499,15 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
       OCCL_DISPATCH(dtype, op, move_slice, prim, src, cin, dst, cout, nelem, ctid, cnt);
     } else {
       const bool disc = discard && (prim & A_RECV) && !(prim & A_DIN) && !((uintptr_t)cin & 127);
+      // l2Hints == 3: a direct receive we forward was stored evict-last by the upstream
+      const bool demote = l2 >= 3 && (prim & A_DIN) && (prim & A_SEND) && !((uintptr_t)cin & 127);
       for (int off = 0; off < vb; off += kTile) {
         const uint32_t s = cs;
         mbar_wait(&tfull[s], cph);
         if (++cs == S) { cs = 0; cph ^= 1; }
         const int sz = min(kTile, vb - off);
         if (disc && ctid < (sz >> 7)) discard_l2_line(cin + off + ((size_t)ctid << 7));  // tile is in smem now
+        if (demote && ctid < (sz >> 7)) demote_l2_line(cin + off + ((size_t)ctid << 7));   // kept by the upstream
         if (bulk) {
           // bulk-store mode: reduce in place in shared memory; the publisher lane
           // stores the tile with cp.async.bulk (copy tiles need no compute at all)
@@ -1470,9 +1522,9 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
           continue;
         }
         if (prim & A_REDUCE) {
-          OCCL_DISPATCH(dtype, op, consume_tile, prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol, keep, polKeep);
+          OCCL_DISPATCH(dtype, op, consume_tile, prim, dst + off, cout + off, stages[s], sz, ctid, cnt, l2, pol, polKeep);
         } else {
-          consume_tile<kI32, kSum>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, hints, pol, keep, polKeep);   // copy only
+          consume_tile<kI32, kSum>(prim, dst + off, cout + off, stages[s], sz, ctid, cnt, l2, pol, polKeep);   // copy only
         }
         // every lane releases its own reads of the tile to the producer's next TMA
         // load into it (direct ordering; measured free vs one elected lane)
@@ -1650,6 +1702,7 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
     sh.curId = -1;
     sh.cycRun = sh.cycPoll = sh.cycAcqFence = sh.cycRelFence = sh.nCommit = 0;
     sh.cycCtxLoad = sh.nCtxLoad = sh.cycCtxSave = sh.nCtxSave = 0;
+    sh.cycCqe = sh.nCqe = 0;
     for (uint32_t i = 0; i < sh.qlen; ++i) {
       m.tq[i] = p.tqSave[(size_t)b * p.maxColl + i];
       const int c = (int)(m.tq[i] & 0xffffu);

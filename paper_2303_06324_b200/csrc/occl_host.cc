@@ -124,8 +124,16 @@ struct occlComm {
   SqeWire* sqDev = nullptr;
   uint64_t* sqCurHost = nullptr;
   uint64_t* sqCurDev = nullptr;
-  uint64_t* cqHost = nullptr;
-  uint64_t* cqDev = nullptr;
+  uint64_t* cqHost = nullptr;                    // [maxColl] last completed subSeq (device-written in
+  uint64_t* cqDev = nullptr;                     //   cqMode 0, poller-maintained in the ring modes)
+  uint64_t* cqRingHost = nullptr;                // ring CQ (cqMode 1 / 2): entries + vanilla tail
+  uint64_t* cqRingDev = nullptr;
+  uint64_t* cqTailHost = nullptr;
+  uint64_t* cqTailDev = nullptr;
+  uint64_t* cqReserve = nullptr;                 // device: next ring slot
+  uint32_t cqDepth = 0;
+  uint64_t cqHead = 0;                           // poller: next ring entry to read
+  std::mutex cqMu;
   std::atomic<uint64_t> sqTail{0};
   // per-collective host state
   // per collId: submission token = subSeq << 1 | in-flight bit.  Completion
@@ -240,12 +248,38 @@ occlResult_t launch_locked(Launcher* L) {
   return occlSuccess;
 }
 
+// Ring CQ modes: the poller drains CQEs (collective ids) into the per-id
+// completion counters; one CQE per submission, so the counter equals the subSeq
+// of the last completed submission, as the id-slot CQ reports it directly.
+void drain_cq(occlComm* c) {
+  if (c->cfg.cqMode == 0) return;
+  std::lock_guard<std::mutex> g(c->cqMu);
+  volatile uint64_t* ring = c->cqRingHost;
+  volatile uint64_t* cq = c->cqHost;
+  for (;;) {
+    const uint64_t h = c->cqHead;
+    uint64_t id;
+    if (c->cfg.cqMode == 2) {
+      const uint64_t e = ring[h % c->cqDepth];
+      if ((e >> 32) != ((h + 1) & 0xffffffffull)) break;       // stamp: written for this slot?
+      id = e & 0xffffffffull;
+    } else {
+      if (h >= *reinterpret_cast<volatile uint64_t*>(c->cqTailHost)) break;
+      std::atomic_thread_fence(std::memory_order_acquire);
+      id = ring[h % c->cqDepth];
+    }
+    if (id < (uint64_t)c->cfg.maxColl) cq[id] = cq[id] + 1;
+    c->cqHead = h + 1;
+  }
+}
+
 inline bool tok_inflight(uint64_t t) { return (t & 1) != 0; }
 inline uint64_t tok_seq(uint64_t t) { return t >> 1; }
 
 bool try_complete(occlComm* c, int id) {
   uint64_t t = c->tok[id].load(std::memory_order_acquire);
   if (!tok_inflight(t)) return false;
+  drain_cq(c);
   const uint64_t done = reinterpret_cast<volatile uint64_t*>(c->cqHost)[id];
   if (done < tok_seq(t)) return false;
   // complete exactly the submission observed: fails if the id was completed and
@@ -356,7 +390,8 @@ occlResult_t validate_config(const occlConfig_t& c) {
   if (c.pipeDepth < 1 || c.pipeDepth > 8) return occlInvalidArgument;
   if (c.prefetchSlices < 0 || c.prefetchSlices > 64) return occlInvalidArgument;
   if (c.stagingTiles < 1 || c.stagingTiles > 6) return occlInvalidArgument;
-  if (c.l2Hints < 0 || c.l2Hints > 2) return occlInvalidArgument;
+  if (c.l2Hints < 0 || c.l2Hints > 3) return occlInvalidArgument;
+  if (c.cqMode < 0 || c.cqMode > 2) return occlInvalidArgument;
   if (c.blocksPerSM < 1 || c.blocksPerSM > 2) return occlInvalidArgument;
   if (c.traceCap > (1u << 24)) return occlInvalidArgument;
   if (c.llSliceBytes < 8 || c.llSliceBytes % 8 || c.llSliceBytes > (1u << 20)) return occlInvalidArgument;
@@ -483,6 +518,9 @@ void free_comm(occlComm* c) {
   if (c->sqHost) cudaFreeHost(c->sqHost);
   if (c->sqCurHost) cudaFreeHost(c->sqCurHost);
   if (c->cqHost) cudaFreeHost(c->cqHost);
+  if (c->cqRingHost) cudaFreeHost(c->cqRingHost);
+  if (c->cqTailHost) cudaFreeHost(c->cqTailHost);
+  if (c->cqReserve) cudaFree(c->cqReserve);
   if (c->statsStream) cudaStreamDestroy(c->statsStream);
 }
 
@@ -617,6 +655,18 @@ occlResult_t occlCommCreate(occlComm_t* out, int nranks, int rank, int cudaDev, 
   if ((e = cudaHostAlloc(&cp->cqHost, M * sizeof(uint64_t), flags)) != cudaSuccess) return fail(e);
   std::memset(cp->cqHost, 0, M * sizeof(uint64_t));
   if ((e = cudaHostGetDevicePointer(&cp->cqDev, cp->cqHost, 0)) != cudaSuccess) return fail(e);
+  if (cfg.cqMode != 0) {
+    // ring CQ: depth >= maxColl -- at most one CQE per in-flight id, so it never fills
+    cp->cqDepth = (uint32_t)(2 * M);
+    if ((e = cudaHostAlloc(&cp->cqRingHost, cp->cqDepth * sizeof(uint64_t), flags)) != cudaSuccess) return fail(e);
+    std::memset(cp->cqRingHost, 0, cp->cqDepth * sizeof(uint64_t));
+    if ((e = cudaHostGetDevicePointer(&cp->cqRingDev, cp->cqRingHost, 0)) != cudaSuccess) return fail(e);
+    if ((e = cudaHostAlloc(&cp->cqTailHost, sizeof(uint64_t), flags)) != cudaSuccess) return fail(e);
+    *cp->cqTailHost = 0;
+    if ((e = cudaHostGetDevicePointer(&cp->cqTailDev, cp->cqTailHost, 0)) != cudaSuccess) return fail(e);
+    if ((e = cudaMalloc(&cp->cqReserve, sizeof(uint64_t))) != cudaSuccess) return fail(e);
+    if ((e = cudaMemset(cp->cqReserve, 0, sizeof(uint64_t))) != cudaSuccess) return fail(e);
+  }
   if ((e = cudaStreamCreateWithFlags(&cp->statsStream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(e);
   *out = c.release();
@@ -724,6 +774,11 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   p.mirrorTail = c->mirrorTail;
   p.fetchLock = reinterpret_cast<uint32_t*>(c->mirrorTail + 1);
   p.cqDone = c->cqDev;
+  p.cqMode = c->cfg.cqMode;
+  p.cqDepth = c->cqDepth;
+  p.cqReserve = c->cqReserve;
+  p.cqRing = c->cqRingDev;
+  p.cqTail = c->cqTailDev;
   p.blk = c->blk;
   p.tqSave = c->tqSave;
   p.ctx = c->ctx;
@@ -1107,6 +1162,8 @@ occlResult_t occlGetProbes(occlComm_t c, occlProbes_t* out) {
     out->nCtxLoad += b.nCtxLoad;
     out->cycCtxSave += b.cycCtxSave;
     out->nCtxSave += b.nCtxSave;
+    out->cycCqe += b.cycCqe;
+    out->nCqe += b.nCqe;
     out->cycData += b.cycData;
     out->cycDataWait += b.cycDataWait;
     out->nData += b.nData;
@@ -1168,7 +1225,8 @@ occlResult_t occlGetFootprint(occlComm_t c, occlFootprint_t* out) {
                (size_t)G * c->cfg.traceCap * sizeof(TraceRec) + G * sizeof(uint32_t) +
                (c->ringsDev ? kMaxRings * sizeof(RingDesc) : 0);
   out->device = out->connectorData + out->connectorFlags + out->llLines + out->contexts + out->other;
-  out->pinnedHost = c->cfg.sqDepth * sizeof(SqeWire) + G * sizeof(uint64_t) + M * sizeof(uint64_t);
+  out->pinnedHost = c->cfg.sqDepth * sizeof(SqeWire) + G * sizeof(uint64_t) + M * sizeof(uint64_t) +
+                    (c->cqDepth ? (c->cqDepth + 1) * sizeof(uint64_t) : 0);
   out->perBlockPerColl = (double)(out->device) / (double)(M * G);
   return occlSuccess;
 }

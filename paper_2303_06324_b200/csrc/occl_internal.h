@@ -162,6 +162,7 @@ struct alignas(16) BlockStat {  // per block
   unsigned long long nCommit;       // slices committed
   unsigned long long cycCtxLoad, nCtxLoad;   // context loads (cache misses) by the control lane
   unsigned long long cycCtxSave, nCtxSave;   // lazy dynamic-context saves
+  unsigned long long cycCqe, nCqe;           // CQE write: from the completing increment to the host store issued
 };
 
 // Device event trace (one ring of `traceCap` records per block, %globaltimer
@@ -227,6 +228,14 @@ struct DaemonParams {
   uint32_t* quitWord;               // device, per launch: quit votes | latch (zeroed before each launch)
   uint32_t quitTotal;               // blocks of the launch (G x fused members)
   uint64_t stallNs;                 // FIFO: all entries stuck when none progressed for this long (0: off)
+  // CQ variant (NEXT-3 ablation): 0 = id slots (cqDone, default),
+  // 1 = vanilla MPSC ring (entry, fence, in-order tail update), 2 = packed 64-bit
+  // ring entries {stamp, id} (one host write, no fence between entry and tail)
+  int cqMode;
+  uint32_t cqDepth;                 // ring entries (>= maxColl: one CQE per in-flight id, never full)
+  uint64_t* cqReserve;              // device: next ring slot (gpu-scope atomic)
+  volatile uint64_t* cqRing;        // mapped host [cqDepth]
+  volatile uint64_t* cqTail;        // mapped host: vanilla ring tail (entries published in order)
 };
 
 }  // namespace occl

@@ -55,7 +55,7 @@ class occlConfig_t(C.Structure):
         ("directMode", C.c_int), ("stagingTiles", C.c_int), ("blocksPerSM", C.c_int), ("traceCap", C.c_uint32),
         ("llSliceBytes", C.c_uint32), ("llMaxBytes", C.c_uint32), ("spinNs", C.c_uint32),
         ("bulkStores", C.c_int), ("directRead", C.c_int), ("stallNs", C.c_uint64),
-        ("forceSysScope", C.c_int),
+        ("forceSysScope", C.c_int), ("cqMode", C.c_int),
     ]
 
 
@@ -80,7 +80,7 @@ class occlFootprint_t(C.Structure):
 class occlProbes_t(C.Structure):
     _fields_ = [(k, C.c_uint64) for k in ("cycRun", "cycPoll", "cycAcqFence", "cycRelFence", "cycData",
                                           "cycDataWait", "nData", "nCommit", "nFence", "cycCtxLoad",
-                                          "nCtxLoad", "cycCtxSave", "nCtxSave")]
+                                          "nCtxLoad", "cycCtxSave", "nCtxSave", "cycCqe", "nCqe")]
 
 
 CALLBACK = C.CFUNCTYPE(None, C.c_int, C.c_void_p)

@@ -58,7 +58,7 @@ def test_config_defaults_and_validation():
     for kw in (dict(llSliceBytes=12), dict(llSliceBytes=0), dict(spinNs=0), dict(stagingTiles=7),
                dict(blocksPerSM=3), dict(blocksPerSM=2, blockThreads=608), dict(blockThreads=96),
                dict(blockThreads=640), dict(pipeDepth=9), dict(spinBase=10, spinMin=20), dict(sliceBytes=100),
-               dict(traceCap=1 << 25), dict(l2Hints=3), dict(l2Hints=-1)):
+               dict(traceCap=1 << 25), dict(l2Hints=4), dict(l2Hints=-1)):
         with pytest.raises(occl.OcclError) as e:
             occl.occlCommCreate(2, 0, 0, occl.occlConfigDefault(**kw))
         assert e.value.code == occl.occlInvalidArgument, kw

@@ -208,3 +208,27 @@ occl.destroy_group(comms)
 ''' % (ROOT, os.path.join(ROOT, 'tests'))
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120, cwd=ROOT)
     assert "FIG1C_OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("cq_mode", [1, 2])
+def test_cq_ring_variants(occl_mod, cq_mode):
+    """The paper's ring-buffer CQs as ablations of the id-slot
+    CQ: vanilla (entry, fence, in-order tail) and packed 64-bit {stamp, id}.
+    Random per-rank orders with forced preemption; results exact, one CQE per
+    submission, the CQE-write probe counts them."""
+    comms = occl_mod.local_group(4, 0, **BASE, cqMode=cq_mode, spinBase=8, spinStep=1, spinMin=1, spinCap=32)
+    try:
+        rng = random.Random(cq_mode)
+        kinds = ["allreduce", "allgather", "reducescatter", "broadcast"]
+        colls = [workloads.Coll(i, kinds[i % 4], "f32", rng.randint(1, 30_000), root=i % 4) for i in range(12)]
+        for it in range(4):
+            orders = [rng.sample(range(12), 12) for _ in range(4)]
+            _run_orders(comms, colls, orders, seed=50 + it)
+        for c in comms:
+            c.exit()                                          # probes are flushed when the blocks exit
+        comms[0].quiesce(U.WAIT_S)
+        for c in comms:
+            st, pr = c.stats(), c.probes()
+            assert st["cqeWritten"] == 48 and pr["nCqe"] == 48 and pr["cycCqe"] > 0
+    finally:
+        occl_mod.destroy_group(comms)
