@@ -462,6 +462,7 @@ constexpr int kTile = 16384;           // TMA staging tile (bytes per operand)
 constexpr int kMaxStages = 6;          // staging ring depth: up to 6 x 2 x 16 KiB of loads in flight
 constexpr int kTmaMinBytes = 16384;    // slices below this use register loads (latency-bound sizes)
 constexpr uint32_t kQuitLatch = 0x80000000u;   // quitWord: every block of the launch voted to quit
+constexpr uint64_t kSqPollNs = 2000;           // a blocked collective polls the SQ at most this often
 
 // Scheduler state of one block; touched only by the control thread.
 struct Sched {
@@ -980,7 +981,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   uint64_t headSeen = 0, creditSeen = 0;
   // spins are counted in time: T x spinNs of failed polling (R1) --
   // an LL poll (a 16-B line in L2) and a cached head poll differ 10x in cost
-  uint64_t T = sh.T, spinStart = 0;
+  uint64_t T = sh.T, spinStart = 0, lastSqPoll = 0;
   const uint64_t spinNs = p.spinNs;
   unsigned long long nSlices = 0, cPoll = 0;
   const long long tRun = clock64();
@@ -1092,7 +1093,22 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
       cPoll += clock64() - tp;
       const uint64_t now = globaltimer();
       if (spinStart == 0) spinStart = now;
-      if (now - spinStart > T * spinNs) {                // two-phase blocking: preempt
+      // Priority policy, "checking the SQ more frequently": a
+      // collective blocked for longer than the minimal threshold yields as soon
+      // as new SQEs are there, so the scheduler admits and sorts them before any
+      // entry runs again.  The blocked control thread polls the SQ itself --
+      // otherwise no block of a rank whose collectives all wait would fetch it.
+      bool yieldSq = false;
+      if (p.orderPolicy == 1 && now - spinStart > (uint64_t)p.spinMin * spinNs && now - lastSqPoll > kSqPollNs) {
+        lastSqPoll = now;
+        uint64_t tail = ld_acquire(p.mirrorTail, 0);
+        if (tail <= sh.cursor) {
+          sq_fetch(p, m, b);
+          tail = ld_acquire(p.mirrorTail, 0);
+        }
+        yieldSq = tail > sh.cursor;
+      }
+      if (yieldSq || now - spinStart > T * spinNs) {     // two-phase blocking: preempt
         while (committed != issued) {                    // drain the pipe
           mbar_wait(&pipe.empty[committed % D], (committed / D) & 1);
           commit(committed % D);

@@ -39,6 +39,13 @@ def test_sass_is_sm100a_and_uses_peer_flags():
     # 128-bit global loads/stores on the data path, system/gpu-scope fences for commit visibility
     assert "LDG.E.128" in out and "STG.E.128" in out
     assert "MEMBAR" in out or "FENCE" in out
+    # the TMA staging path: bulk copies global -> shared (cp.async.bulk, SASS UBLKCP.S.G) completing on
+    # mbarriers (SYNCS.ARRIVE.TRANS64 / SYNCS.PHASECHK.TRANS64.TRYWAIT), the bulk-store option
+    # (UBLKCP.G.S), and the L2 discard / priority maintenance of connector lines (CCTL.E.*L2)
+    daemon = out[out.index("occl_daemon_kernel"):]
+    for mnem in ("UBLKCP.S.G", "UBLKCP.G.S", "SYNCS.ARRIVE.TRANS64", "SYNCS.PHASECHK.TRANS64.TRYWAIT",
+                 "CCTL.E.DML2"):
+        assert daemon.count(mnem) >= 2, mnem
 
 
 def test_config_defaults_and_validation():
