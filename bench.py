@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--blocks-per-sm", type=int, default=1)
     ap.add_argument("--bulk-stores", type=int, default=0)
     ap.add_argument("--direct-read", type=int, default=1)
+    ap.add_argument("--order-policy", type=int, default=1)
+    ap.add_argument("--sq-yield-ns", type=int, default=-1, help="-1: library default")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--check", action="store_true", help="sampled oracle check of the timed output")
@@ -223,7 +225,10 @@ def bench_cfg(args, **extra):
               slicesPerChunk=args.slices_per_chunk, blockThreads=args.threads, pipeDepth=args.pipe_depth,
               prefetchSlices=args.prefetch, discardConsumed=args.discard, l2Hints=args.l2_hints,
               directMode=args.direct, stagingTiles=args.stages, blocksPerSM=args.blocks_per_sm,
-              bulkStores=args.bulk_stores, directRead=args.direct_read, maxColl=128, autoLaunch=0)
+              bulkStores=args.bulk_stores, directRead=args.direct_read, maxColl=128, autoLaunch=0,
+              orderPolicy=args.order_policy)
+    if args.sq_yield_ns >= 0:
+        kw["sqYieldNs"] = args.sq_yield_ns
     kw.update(extra)
     return occl.occlConfigDefault(**kw)
 

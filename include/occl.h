@@ -124,6 +124,9 @@ typedef struct {
                              data path, selectable on one device for testing and benchmarking */
   int cqMode;             /* CQ variant: 0 = one slot per collId (default), 1 = vanilla
                              MPSC ring (entry, fence, in-order tail), 2 = packed 64-bit {stamp, id} ring */
+  uint64_t sqYieldNs;     /* priority policy: a collective blocked on a peer for >= spinMin spins yields to
+                             newly submitted SQEs; its rank polls the host SQ for them at most once per
+                             sqYieldNs (0 = never: new SQEs are seen only between runs) */
 } occlConfig_t;
 
 /* Aggregate counters (device counters summed over blocks/collectives). */

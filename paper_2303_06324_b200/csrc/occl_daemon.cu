@@ -472,6 +472,7 @@ struct Sched {
   uint32_t rr;                 // priority policy: next non-front entry to visit
   uint32_t voted;              // this block voted for the launch's voluntary quit
   uint64_t lastProgress;       // %globaltimer of the last run that committed a slice
+  uint64_t lastSqPoll;         // %globaltimer of this block's last SQ check while blocked (priority policy)
   int lastRun, curId;
   int way;
   unsigned long long cycRun, cycPoll, cycAcqFence, cycRelFence, nCommit;   // probes
@@ -961,10 +962,10 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   // direct-read slice, and we hold RUN_DONE until then (a failed ack poll is a
   // spin: preemptible like any connector wait).  An all-reduce needs no ack:
   // its final Recv carries data the downstream produced after its direct read.
+  // (the ack addresses are recomputed where used: keeping them live costs the
+  // control thread registers it spills in its hot loop)
   const bool dreadUp = dRead && dOut && n > 1 && kind == kReduceScatter;     // downstream reads our buffer
   const bool dreadDown = dRead && dIn && n > 1 && kind == kReduceScatter;    // we read our upstream's
-  const char* ackIn = p.flagsLocal + cb * kFlagStride + kDirectOff + 32;
-  char* ackOut = R.flagsPrev + cb * kFlagStride + kDirectOff + 32;
   uint64_t peerSrc = 0;                                   // upstream's send buffer (direct read)
   const uint64_t subSeq = cx.s.subSeq;
   uint64_t peerRecv = 0;                                  // downstream's recv buffer (direct sends)
@@ -981,7 +982,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   uint64_t headSeen = 0, creditSeen = 0;
   // spins are counted in time: T x spinNs of failed polling (R1) --
   // an LL poll (a 16-B line in L2) and a cached head poll differ 10x in cost
-  uint64_t T = sh.T, spinStart = 0, lastSqPoll = 0;
+  uint64_t T = sh.T, spinStart = 0;
   const uint64_t spinNs = p.spinNs;
   unsigned long long nSlices = 0, cPoll = 0;
   const long long tRun = clock64();
@@ -991,6 +992,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   auto commit = [&](uint32_t slot) {
     const int cp = pipe.ring[slot].prim;
     if (dreadDown && (cp & A_DREAD) && dc.loop + 1 == nloops && dc.slc + 1 == (uint32_t)spc) {
+      char* ackOut = p.rings[cx.sub].flagsPrev + cb * kFlagStride + kDirectOff + 32;
       if (sys) asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(ackOut), "l"(subSeq) : "memory");
       else asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(ackOut), "l"(subSeq) : "memory");
     }
@@ -1013,7 +1015,10 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     }
     if (di.loop >= nloops) {                              // everything issued
       if (committed != issued) continue;
-      if (!dreadUp || ld_acquire(ackIn, sys) == subSeq) { run = RUN_DONE; break; }
+      if (!dreadUp || ld_acquire(p.flagsLocal + cb * kFlagStride + kDirectOff + 32, sys) == subSeq) {
+        run = RUN_DONE;
+        break;
+      }
       // the downstream has not finished reading our send buffer: a failed poll
       const uint64_t now = globaltimer();
       if (spinStart == 0) spinStart = now;
@@ -1096,17 +1101,30 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
       // Priority policy, "checking the SQ more frequently": a
       // collective blocked for longer than the minimal threshold yields as soon
       // as new SQEs are there, so the scheduler admits and sorts them before any
-      // entry runs again.  The blocked control thread polls the SQ itself --
-      // otherwise no block of a rank whose collectives all wait would fetch it.
+      // entry runs again.  A blocked control thread looks at the device mirror
+      // (an L2 read) every kSqPollNs; the host SQ itself is peeked (ONE 16-B
+      // PCIe load: the stamp of the next unfetched slot) by at most one blocked
+      // block of the rank per sqYieldNs -- otherwise no block of a rank whose
+      // collectives all wait would see new SQEs.  The scheduler fetches them
+      // after the yield.  No call here: a call in this loop makes the control
+      // thread spill its live state around it (measured -27 % bench busbw).
       bool yieldSq = false;
-      if (p.orderPolicy == 1 && now - spinStart > (uint64_t)p.spinMin * spinNs && now - lastSqPoll > kSqPollNs) {
-        lastSqPoll = now;
-        uint64_t tail = ld_acquire(p.mirrorTail, 0);
-        if (tail <= sh.cursor) {
-          sq_fetch(p, m, b);
-          tail = ld_acquire(p.mirrorTail, 0);
+      if (p.orderPolicy == 1 && p.sqYieldNs && now - spinStart > (uint64_t)p.spinMin * spinNs &&
+          now - sh.lastSqPoll > kSqPollNs) {
+        sh.lastSqPoll = now;
+        const uint64_t tail = ld_acquire(p.mirrorTail, 0);
+        if (tail > sh.cursor) {
+          yieldSq = true;
+        } else {
+          unsigned long long* lastHost = reinterpret_cast<unsigned long long*>(p.mirrorTail + 3);
+          const unsigned long long lh = *reinterpret_cast<volatile unsigned long long*>(lastHost);
+          if (now - lh > p.sqYieldNs && atomicCAS(lastHost, lh, (unsigned long long)now) == lh) {
+            uint32_t stamp;
+            asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(stamp) : "l"(p.sq[tail % p.sqDepth].c[0])
+                         : "memory");
+            yieldSq = stamp == (uint32_t)(tail + 1);
+          }
         }
-        yieldSq = tail > sh.cursor;
       }
       if (yieldSq || now - spinStart > T * spinNs) {     // two-phase blocking: preempt
         while (committed != issued) {                    // drain the pipe
@@ -1714,6 +1732,7 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
     sh.rr = 1;
     sh.voted = 0;
     sh.lastProgress = 0;
+    sh.lastSqPoll = 0;
     sh.lastRun = -1;
     sh.curId = -1;
     sh.cycRun = sh.cycPoll = sh.cycAcqFence = sh.cycRelFence = sh.nCommit = 0;

@@ -589,6 +589,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->llMaxBytes = 64 << 10;
   c->blocksPerSM = 1;
   c->l2Hints = 2;
+  c->sqYieldNs = 20'000;
   return occlSuccess;
 }
 
@@ -628,8 +629,8 @@ occlResult_t occlCommCreate(occlComm_t* out, int nranks, int rank, int cudaDev, 
   if ((e = cudaMemset(cp->ctx, 0, M * G * sizeof(CtxSlot))) != cudaSuccess) return fail(e);
   if ((e = cudaMalloc(&cp->sqMirror, cfg.sqDepth * sizeof(Sqe))) != cudaSuccess) return fail(e);
   // tail, fetch lock, cached minimum block cursor
-  if ((e = cudaMalloc(&cp->mirrorTail, 3 * sizeof(uint64_t))) != cudaSuccess) return fail(e);
-  if ((e = cudaMemset(cp->mirrorTail, 0, 3 * sizeof(uint64_t))) != cudaSuccess) return fail(e);
+  if ((e = cudaMalloc(&cp->mirrorTail, 4 * sizeof(uint64_t))) != cudaSuccess) return fail(e);
+  if ((e = cudaMemset(cp->mirrorTail, 0, 4 * sizeof(uint64_t))) != cudaSuccess) return fail(e);
   if ((e = cudaMalloc(&cp->blk, G * sizeof(BlockState))) != cudaSuccess) return fail(e);
   if ((e = cudaMemset(cp->blk, 0, G * sizeof(BlockState))) != cudaSuccess) return fail(e);
   if ((e = cudaMalloc(&cp->tqSave, G * M * sizeof(uint32_t))) != cudaSuccess) return fail(e);
@@ -833,6 +834,7 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   p.blocksPerSM = c->cfg.blocksPerSM;
   p.l2Hints = c->cfg.l2Hints;
   p.stallNs = c->cfg.stallNs;
+  p.sqYieldNs = c->cfg.sqYieldNs;
   Launcher* L = new Launcher();
   if ((r = launcher_start(L, {c})) != occlSuccess) {
     launcher_stop(L);

@@ -183,7 +183,8 @@ struct DaemonParams {
   const SqeWire* sq;                // mapped host SQ (stamped wire format)
   volatile uint64_t* sqCursorHost;  // mapped host [G]: [0] = SQEs copied to the mirror (slots below are free)
   Sqe* sqMirror;                    // device [sqDepth]: copy of the host SQ read by every block
-  uint64_t* mirrorTail;             // device: [0] SQEs in the mirror, [1] fetch lock, [2] cached min block cursor
+  uint64_t* mirrorTail;             // device: [0] SQEs in the mirror, [1] fetch lock, [2] cached min block cursor,
+                                    //         [3] %globaltimer of the last host-SQ poll by a blocked collective
   uint32_t* fetchLock;              // device: the block copying host SQEs holds it
   volatile uint64_t* cqDone;        // mapped host [maxColl]: last completed subSeq
   BlockState* blk;                  // [G]
@@ -228,6 +229,7 @@ struct DaemonParams {
   uint32_t* quitWord;               // device, per launch: quit votes | latch (zeroed before each launch)
   uint32_t quitTotal;               // blocks of the launch (G x fused members)
   uint64_t stallNs;                 // FIFO: all entries stuck when none progressed for this long (0: off)
+  uint64_t sqYieldNs;               // priority: host-SQ poll period of blocked collectives (0: no yield)
   // CQ variant (NEXT-3 ablation): 0 = id slots (cqDone, default),
   // 1 = vanilla MPSC ring (entry, fence, in-order tail update), 2 = packed 64-bit
   // ring entries {stamp, id} (one host write, no fence between entry and tail)
