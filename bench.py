@@ -44,7 +44,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 MiB = 1 << 20
-METRIC = "allreduce bus GB/s (8-rank ring, fp32 sum)"
+METRIC = "allreduce bus GB/s (ring AllReduce, sum; ring size and dtype in config)"
 
 
 def parse():
@@ -169,6 +169,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    if not args.ranks:                     # the OCCL arm's ring: 8 virtual ranks at N=1, one rank per GPU above
+        args.ranks = args.gpus if args.gpus > 1 else 8
     size = int(args.size_mib * MiB)
     from inputs import hashgen
     from oracle import ring
@@ -188,7 +190,8 @@ def run_reference(args):
     unit = "GB/s"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": unit, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak" if args.gpus > 1 else "strong",
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (counter-based hash generator)",
         "config": {"workload": f"C2 allreduce, {args.ranks}-rank ring, {args.size_mib:g} MiB/rank {args.dtype} sum",
                    "ranks": args.ranks, "size_bytes_per_rank": size},
@@ -217,6 +220,19 @@ def setup_dist(args):
         os.environ.setdefault("NCCL_PROTO", "Simple")
         dist.init_process_group(os.environ.get("OCCL_BENCH_BACKEND", "nccl"), init_method="env://")
     return world, rank, local, dist
+
+
+def summarize_probes(pb, pa):
+    """In-kernel probe deltas (occlGetProbes) summed over the local ranks, per slice / fence."""
+    probes = {k: sum(a[k] - b[k] for a, b in zip(pa, pb)) for k in pa[0]}
+    nc, nd = max(1, probes["nCommit"]), max(1, probes["nData"])
+    return {"per_commit_cycles": {k: round(probes[k] / nc, 1) for k in ("cycRun", "cycPoll", "cycAcqFence",
+                                                                        "cycRelFence")},
+            "per_slice_data_cycles": round(probes["cycData"] / nd, 1),
+            "per_slice_datawait_cycles": round(probes["cycDataWait"] / nd, 1),
+            "commits": probes["nCommit"], "data_slices_timed": probes["nData"],
+            "publisher_fences": probes["nFence"],
+            "cycles_per_release_fence": round(probes["cycRelFence"] / max(1, probes["nFence"]), 1)}
 
 
 def bench_cfg(args, **extra):
@@ -343,15 +359,7 @@ def run_single(args, world, prank, local, dist):
     barrier()
     after = [c.stats() for c in comms]
     pa = [c.probes() for c in comms]
-    probes = {k: sum(a[k] - b[k] for a, b in zip(pa, pb)) for k in pa[0]}
-    nc, nd = max(1, probes["nCommit"]), max(1, probes["nData"])
-    probe_summary = {"per_commit_cycles": {k: round(probes[k] / nc, 1) for k in
-                                           ("cycRun", "cycPoll", "cycAcqFence", "cycRelFence")},
-                     "per_slice_data_cycles": round(probes["cycData"] / nd, 1),
-                     "per_slice_datawait_cycles": round(probes["cycDataWait"] / nd, 1),
-                     "commits": probes["nCommit"], "data_slices_timed": probes["nData"],
-                     "publisher_fences": probes["nFence"],
-                     "cycles_per_release_fence": round(probes["cycRelFence"] / max(1, probes["nFence"]), 1)}
+    probe_summary = summarize_probes(pb, pa)
     if dist is not None:
         t = torch.tensor([ms_total], dtype=torch.float64, device=_red_dev(dist, dev))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -502,7 +510,9 @@ def conn_only_variant(args, dev, sends, recvs, size, peaks):
     try:
         timed_launch(comms, sends, recvs, max(3, args.warmup), stream)
         steps = max(5, args.steps)
+        pb = [c.probes() for c in comms]
         ms = timed_launch(comms, sends, recvs, steps, stream, first_id=50) / steps
+        probes = summarize_probes(pb, [c.probes() for c in comms])
     finally:
         occl.destroy_group(comms)
     bw = busbw(size, R, ms / 1e3)
@@ -510,7 +520,7 @@ def conn_only_variant(args, dev, sends, recvs, size, peaks):
     peak = peaks.get("hbm_gbs", 6650.0)
     return {"value": bw, "unit": "GB/s", "ms_per_step": ms, "steps": steps,
             "config": "forceSysScope=1: connector-only edges, .sys fences / flags (directMode, directRead off)",
-            "roofline_frac": alg / peak, "vs_direct_mode": None}
+            "roofline_frac": alg / peak, "vs_direct_mode": None, "probes": probes}
 
 
 # ============================================================================ N >= 2: one rank per GPU
@@ -568,6 +578,45 @@ def nccl_allreduce_ms(dist, group, t, steps, warmup):
     e1.record()
     e1.synchronize()
     return e0.elapsed_time(e1) / steps
+
+
+def multi_e2e(args, comm, send, recv, size, dist, dev):
+    """End to end through the public API at N GPUs: per step, the H2D copy of this
+    rank's input from pinned host memory, occlAllReduce on the event-driven daemon,
+    occlWait, and the D2H copy of the result; host clock, max over ranks."""
+    import torch
+    host_in = torch.empty(send.numel(), dtype=send.dtype, pin_memory=True)
+    host_in.copy_(send.cpu())
+    host_out = torch.empty(recv.numel(), dtype=recv.dtype, pin_memory=True)
+    comm.set_auto_launch(True)
+    cs = torch.cuda.Stream(device=dev)
+    steps = max(3, min(args.steps, 10))
+
+    def step(k):
+        with torch.cuda.stream(cs):
+            send.copy_(host_in, non_blocking=True)
+        cs.synchronize()
+        cid = 120 + (k % 4)
+        comm.all_reduce(send, recv, cid)
+        comm.wait(cid, 600)
+        with torch.cuda.stream(cs):
+            host_out.copy_(recv, non_blocking=True)
+        cs.synchronize()
+
+    step(0)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for k in range(steps):
+        step(k + 1)
+    te = (time.perf_counter() - t0) / steps
+    t = torch.tensor([te], dtype=torch.float64, device=_red_dev(dist, dev))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    te = float(t.item())
+    comm.set_auto_launch(False)
+    comm.quiesce(600)
+    return {"value": busbw(size, dist.get_world_size(), te), "unit": "GB/s", "h2d_bytes_per_step": size,
+            "d2h_bytes_per_step": size, "ms_per_step": te * 1e3, "steps": steps,
+            "path": "pinned host -> device copy + occlAllReduce (event-driven daemon) + occlWait + D2H, per rank"}
 
 
 def run_multi(args, world, prank, local, dist):
@@ -635,6 +684,8 @@ def run_multi(args, world, prank, local, dist):
                 row[f"nccl_{name}_ms"] = m
                 row[f"nccl_{name}_busbw"] = busbw(size, R, m / 1e3)
                 del x
+            if smib == args.size_mib and not args.no_e2e:
+                row["e2e"] = multi_e2e(args, comm, send, recv, size, dist, dev)
             rows.append(row)
             del send, recv
             torch.cuda.empty_cache()
@@ -667,7 +718,7 @@ def run_multi(args, world, prank, local, dist):
         "clocks": clk.summary(),
         "roofline": roofline,
         "cpu_baseline": None,
-        "e2e": None,
+        "e2e": head.get("e2e"),
         "baseline": baseline or {"nccl": "unavailable: " + ("backend " + backend if backend != "nccl" else
                                                             "fewer GPUs than ranks" if not distinct else "--no-nccl")},
         "ratio_vs_nccl": (value / head["nccl_ring_simple_busbw"]) if "nccl_ring_simple_busbw" in head else None,
