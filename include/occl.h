@@ -202,120 +202,194 @@ typedef void (*occlCallback_t)(int collId, void* arg);
 
 #define OCCL_HANDLE_BYTES 256
 
+/* Static description of a result code.  Never NULL. */
 const char* occlGetErrorString(occlResult_t result);
 
-/* Fill *cfg with defaults. */
+/* Fill *cfg with the library defaults (thresholds of reading R1, slices of 192 KiB,
+ * K = 4 slots, priority order policy).  Errors: occlInvalidArgument (cfg NULL). */
 occlResult_t occlConfigDefault(occlConfig_t* cfg);
 
-/* Create rank `rank` of an `nranks` ring on CUDA device `cudaDev`: allocates the
- * connector arena (maxColl x G x K x sliceBytes data + flags), context buffer,
- * completion counters (device memory) and the SQ / CQ / per-block SQ cursors
- * (pinned, mapped host memory).  cfg == NULL => defaults.  Not usable until
- * occlCommConnect. */
+/* --- communicator setup: registration before execution (§3.1.1;
+ *     dedicated connectors per collective and block, §5) ---------- */
+
+/* Create rank `rank` (0 <= rank < nranks <= 64) of an `nranks` ring on CUDA device
+ * `cudaDev`.  Allocates, owned by the communicator: the connector arena
+ * (maxColl x G x K x sliceBytes data + maxColl x G x 384 B flags, device), the
+ * context buffer (maxColl x G x 128 B), completion counters, and the SQ / CQ /
+ * SQ cursors in pinned mapped host memory.  cfg == NULL => occlConfigDefault;
+ * *cfg is copied.  Every rank of a ring must pass identical cfg values.  Not
+ * usable for collectives until occlCommConnect.
+ * Errors: occlInvalidArgument (bad rank/nranks/device, invalid cfg),
+ * occlCudaError (allocation, no such device). */
 occlResult_t occlCommCreate(occlComm_t* comm, int nranks, int rank, int cudaDev,
                             const occlConfig_t* cfg);
 
-/* Serialise this rank's handle (<= OCCL_HANDLE_BYTES bytes) into `out`; *len is
- * in: capacity, out: bytes written.  The handle carries the arena's CUDA IPC
- * handle, its raw device pointer, pid and device (same-process peers use the
- * raw pointer directly). */
+/* Serialise this rank's handle into `out` (caller-owned, *len bytes of
+ * capacity >= OCCL_HANDLE_BYTES); on return *len = bytes written.  The handle is
+ * plain bytes: the arena's CUDA IPC handle, its raw device pointer, pid and
+ * device (a same-process peer uses the raw pointer directly).
+ * Errors: occlInvalidArgument (NULL pointer, capacity too small). */
 occlResult_t occlCommGetHandle(occlComm_t comm, void* out, size_t* len);
 
-/* Open the ring neighbours' arenas from the rank-major array of every rank's
- * handle (lenPerRank bytes each), enable peer access, start the supervisor. */
+/* Open the ring neighbours' arenas (rank r pushes into r+1 and returns credits
+ * to r-1: the send side of r is the receive side of r+1) from
+ * `allHandles`: nranks handles, rank-major, lenPerRank bytes each, caller-owned,
+ * read during the call only.  Enables peer access / opens IPC mappings and
+ * starts the host supervisor thread (poller + event-driven launcher).
+ * Errors: occlInvalidArgument (NULL, short handles, a handle of another ring
+ * geometry), occlInvalidUsage (already connected), occlCudaError (IPC open,
+ * peer access). */
 occlResult_t occlCommConnect(occlComm_t comm, const void* allHandles, size_t lenPerRank);
 
-/* Serve `n` connected communicators of THIS process that live on the same device
- * with ONE daemon kernel launch: blocks [i*G, (i+1)*G) run comms[i]'s daemon,
- * each with its own SQ, CQ, contexts and connectors.  Used for several (virtual)
- * ranks sharing one B200: their daemons are co-resident by construction and are
- * started, stopped and timed together.  All must share gridBlocks, maxColl,
- * cacheWays and blockThreads, be idle and have nothing in flight. */
-occlResult_t occlCommFuse(occlComm_t* comms, int n);
-
-/* Sub-communicator (a collective's static context carries its own
- * nranks / rank, so one daemon per GPU serves collectives of overlapping rank
- * sets).  `members` lists the parent ranks of the new ring in its rank order;
- * every member calls this with the same list (globally agreed, like collId) and
- * the caller must be a member.  The child shares the parent's daemon, SQ, CQ and
- * collId registry; its collectives use dedicated connectors at (collId, block)
- * in the members' arenas, opened from the handles the parent received at
- * occlCommConnect.  A collId is BOUND to the (sub-)communicator of its first
- * submission -- its connector sequence numbers belong to that ring's edges --
- * and submitting it on another returns occlInvalidUsage; destroying a child
- * retires the ids bound to it.  Destroy children before their parent.  Up to
- * 31 live sub-communicators per communicator (a destroyed child's slot is
- * reused). */
-occlResult_t occlCommSplit(occlComm_t parent, int nmembers, const int* members, occlComm_t* child);
-
-/* Create + GetHandle + ag(...) + Connect.  The paper's occlCommInit. */
+/* occlCommCreate + occlCommGetHandle + ag(...) + occlCommConnect: the paper's
+ * registration step over a rank set.  `ag` gathers
+ * OCCL_HANDLE_BYTES from every rank, rank-major, into its `out` (e.g. an MPI or
+ * torch.distributed all-gather); it is called once, synchronously, with agCtx.
+ * Errors: those of the three calls; occlSystemError if ag returns non-zero (the
+ * half-built communicator is destroyed, *comm untouched). */
 occlResult_t occlCommInit(occlComm_t* comm, int nranks, int rank, int cudaDev,
                           occlAllGatherFn ag, void* agCtx, const occlConfig_t* cfg);
 
-/* Push the Exiting SQE, wait for the daemon to drain and exit,
- * free everything.  occlInvalidUsage if collectives are still in flight. */
+/* Serve `n` connected communicators of THIS process that live on the same device
+ * with ONE daemon kernel launch: blocks [i*G, (i+1)*G) run comms[i]'s daemon,
+ * each with its own SQ, CQ, contexts and connectors (virtual ranks sharing one
+ * B200: co-resident by construction, started, stopped and timed together).  All
+ * must share gridBlocks, maxColl, cacheWays and blockThreads, be idle and have
+ * nothing in flight.  The array is read during the call only.
+ * Errors: occlInvalidArgument (NULL, n < 1, mismatched geometry or devices),
+ * occlInvalidUsage (not connected, a sub-communicator, already fused, busy). */
+occlResult_t occlCommFuse(occlComm_t* comms, int n);
+
+/* Sub-communicator (§3.1.1: a collective's static context carries
+ * its own nranks / rank, so one daemon per GPU serves collectives of overlapping
+ * rank sets).  `members` (caller-owned, nmembers distinct parent ranks, read
+ * during the call) lists the new ring in its rank order; every member calls this
+ * with the same list (globally agreed, like collId) and the caller must be a
+ * member.  The child shares the parent's daemon, SQ, CQ and collId registry; its
+ * collectives use dedicated connectors at (collId, block) in the members' arenas,
+ * opened from the handles the parent received at occlCommConnect.  A collId is
+ * BOUND to the (sub-)communicator of its first submission -- its connector
+ * sequence numbers belong to that ring's edges -- and submitting it on another
+ * returns occlInvalidUsage; destroying a child retires the ids bound to it.
+ * Destroy children before their parent.  Up to 31 live sub-communicators per
+ * communicator (a destroyed child's slot is reused).
+ * Errors: occlInvalidArgument (NULL, duplicate / out-of-range member, caller not
+ * a member), occlInvalidUsage (parent not a connected root, no free slot),
+ * occlCudaError. */
+occlResult_t occlCommSplit(occlComm_t parent, int nmembers, const int* members, occlComm_t* child);
+
+/* Push the Exiting SQE (§3.1.2), wait for the daemon to drain and
+ * exit, free everything the communicator owns.  A sticky-errored communicator
+ * can still be destroyed.
+ * Errors: occlInvalidArgument (NULL), occlInvalidUsage (collectives still in
+ * flight, or live sub-communicators). */
 occlResult_t occlCommDestroy(occlComm_t comm);
 
-/* Asynchronous submission (one SQE each).  Returns once the SQE is in the SQ. */
+/* --- collectives: asynchronous submission of one SQE = {collective id, send /
+ *     recv buffer addresses, shape} (§3.1.2), any per-rank order
+ *     (§3.1).  Each returns once the SQE is in the SQ (a full SQ
+ *     blocks until the daemon frees a slot); completion is reported by the CQE
+ *     (occlWait / occlTest / occlSetCallback).  Buffers: DEVICE pointers on the
+ *     communicator's device, caller-owned, contiguous, element type `datatype`;
+ *     `send` must hold its data at the call and stay unmodified, and both must stay
+ *     allocated, until local completion.  The ring primitive sequences follow
+ *     NCCL's Ring/Simple; the reduction order is the
+ *     ring's left fold of DESIGN.md R6/R7, so results are bit-exact with oracle O1.
+ * Common errors: occlInvalidArgument (NULL buffer with count > 0, bad datatype /
+ * op / root, collId < 0), occlRegistryFull (collId >= maxColl),
+ * occlDuplicateSubmit (collId still in flight), occlInvalidUsage
+ * (not connected; collId bound to another sub-communicator), occlCudaError
+ * (sticky device fault).  count == 0 completes at submission. */
+
+/* AllReduce: recvbuff[i] = (+) over ranks of sendbuff[i], i < count (count
+ * elements per rank in both buffers; in place iff send == recv). */
 occlResult_t occlAllReduce(const void* sendbuff, void* recvbuff, size_t count,
                            occlDataType_t datatype, occlRedOp_t op, int collId, occlComm_t comm);
+/* AllGather: recvbuff[q*sendcount + j] = rank q's sendbuff[j]; recvbuff holds
+ * nranks*sendcount elements (in place iff send == recv + rank*sendcount). */
 occlResult_t occlAllGather(const void* sendbuff, void* recvbuff, size_t sendcount,
                            occlDataType_t datatype, int collId, occlComm_t comm);
+/* ReduceScatter: recvbuff[j] = (+) over ranks q of q's sendbuff[rank*recvcount + j];
+ * sendbuff holds nranks*recvcount elements (in place iff recv == send + rank*recvcount). */
 occlResult_t occlReduceScatter(const void* sendbuff, void* recvbuff, size_t recvcount,
                                occlDataType_t datatype, occlRedOp_t op, int collId, occlComm_t comm);
+/* Broadcast: every rank's recvbuff = the root's sendbuff (count elements; the
+ * root may pass send == recv).  0 <= root < nranks. */
 occlResult_t occlBroadcast(const void* sendbuff, void* recvbuff, size_t count,
                            occlDataType_t datatype, int root, int collId, occlComm_t comm);
-/* Reduce to `root` (NCCL ring Reduce: the chain root+1 -> ... -> root folds the
- * inputs in that order); only the root's recvbuff is written. */
+/* Reduce (beyond the paper's four, R23): NCCL's ring Reduce, the chain
+ * root+1 -> ... -> root folds the inputs in that order; only the root's recvbuff
+ * (count elements) is written, other ranks' recvbuff may be NULL. */
 occlResult_t occlReduce(const void* sendbuff, void* recvbuff, size_t count, occlDataType_t datatype,
                         occlRedOp_t op, int root, int collId, occlComm_t comm);
 
-/* Block until the latest submission of collId completed locally (its CQE was
- * posted).  timeoutNs < 0 waits forever.  occlUnknownId if never submitted. */
+/* --- completion: CQE, poller, callback map (§3.1.2; the CQ
+ *     variants of PAPER.md:496-506, §4, cfg.cqMode) ---------------------------- */
+
+/* Block until the latest submission of collId completed locally: its CQE was
+ * posted, so this rank's buffers are free (no peer still reads `send` or writes
+ * `recv`).  timeoutNs < 0 waits forever.
+ * Errors: occlInvalidArgument, occlRegistryFull, occlUnknownId (never
+ * submitted), occlTimeout, occlCudaError (sticky fault). */
 occlResult_t occlWait(occlComm_t comm, int collId, int64_t timeoutNs);
 
-/* Non-blocking completion test: *done = 1 when complete. */
+/* Non-blocking completion test: *done = 1 when the latest submission of collId
+ * completed locally, else 0.  Errors: as occlWait, minus occlTimeout. */
 occlResult_t occlTest(occlComm_t comm, int collId, int* done);
 
-/* Bind a callback fired exactly once per completion of collId by the host
- * poller.  cb == NULL unbinds. */
+/* Bind cb(collId, arg), fired exactly once per completion of collId by the host
+ * poller thread; it must not block and must not call back
+ * into this communicator's submit / wait functions.  cb == NULL unbinds.
+ * Errors: occlInvalidArgument, occlRegistryFull, occlInvalidUsage (collId in
+ * flight: rebinding only between submissions). */
 occlResult_t occlSetCallback(occlComm_t comm, int collId, occlCallback_t cb, void* arg);
 
-/* User-defined priority of collId for the priority order policy:
- * lower values run first; the task queues are kept sorted by it.  Like collId it
- * must be globally agreed.  Default: priority = collId.  Takes effect at the
- * next submission of collId. */
+/* User-defined priority of collId for the priority order policy (PAPER.md:438-446,
+ * §3.2; reading R10): lower values run first; the task queues are kept sorted by
+ * it.  Like collId it must be globally agreed.  Default: priority = collId.
+ * Takes effect at the next submission of collId.
+ * Errors: occlInvalidArgument, occlRegistryFull. */
 occlResult_t occlSetPriority(occlComm_t comm, int collId, int32_t priority);
 
-/* Counters (a snapshot; the daemon may be running). */
+/* --- observability (the paper's probes and traces) */
+/* Counters summed over blocks (a snapshot; the daemon may be running); *out is
+ * caller-owned.  Errors: occlInvalidArgument (NULL), occlRegistryFull (collId). */
 occlResult_t occlGetStats(occlComm_t comm, occlStats_t* out);
 occlResult_t occlGetCollStats(occlComm_t comm, int collId, occlCollStats_t* out);
 occlResult_t occlGetProbes(occlComm_t comm, occlProbes_t* out);
 occlResult_t occlGetFootprint(occlComm_t comm, occlFootprint_t* out);
 
 /* Device event trace of block `block` (cfg.traceCap > 0): the most recent
- * min(written, traceCap) records, oldest first, into out[0..cap); *n = count
- * copied.  occlTraceReset forgets everything recorded so far (daemon idle). */
+ * min(written, traceCap) records, oldest first, into the caller's out[0..cap);
+ * *n = count copied.  occlTraceReset forgets everything recorded so far.
+ * Errors: occlInvalidArgument (block out of range, out NULL with cap > 0),
+ * occlInvalidUsage (reset while the daemon runs). */
 occlResult_t occlGetTrace(occlComm_t comm, int block, occlTraceRec_t* out, size_t cap, size_t* n);
 occlResult_t occlTraceReset(occlComm_t comm);
 
-/* --- daemon control (the paper's lifecycle made explicit) --------------------- */
-/* Push an Exiting SQE: every block drains its task queue, then exits.  A later
- * submission restarts the daemon (event-driven start). */
+/* --- daemon lifecycle: voluntary quit and event-driven start (PAPER.md:406-416,
+ *     §3.1.3), made explicit ---------------------------------------------------- */
+/* Push an Exiting SQE: every block drains its task queue, then
+ * exits.  A later submission restarts the daemon (event-driven start).
+ * Errors: occlInvalidArgument, occlInvalidUsage (not connected). */
 occlResult_t occlCommExit(occlComm_t comm);
 /* Launch the daemon now if it is not running (what the supervisor does on an
- * SQE when autoLaunch = 1). */
+ * SQE when autoLaunch = 1).  Refuses a grid that cannot be co-resident.
+ * Errors: occlInvalidArgument, occlInvalidUsage, occlCudaError. */
 occlResult_t occlCommLaunch(occlComm_t comm);
 /* Enable / disable the supervisor's event-driven start.  While it is disabled the
  * daemon does not quit voluntarily either (nobody would restart it): launches
- * made with occlCommLaunch run until their Exiting SQE. */
+ * made with occlCommLaunch run until their Exiting SQE.  Errors: occlInvalidArgument. */
 occlResult_t occlCommSetAutoLaunch(occlComm_t comm, int enable);
-/* Wait until no daemon kernel of this communicator is running. */
+/* Wait until no daemon kernel of this communicator is running (timeoutNs < 0:
+ * forever).  Errors: occlInvalidArgument, occlTimeout, occlCudaError. */
 occlResult_t occlCommQuiesce(occlComm_t comm, int64_t timeoutNs);
-/* The CUDA stream (cudaStream_t) the daemon kernel is launched on. */
+/* The CUDA stream (cudaStream_t, owned by the communicator) the daemon kernel is
+ * launched on.  Errors: occlInvalidArgument. */
 occlResult_t occlCommGetStream(occlComm_t comm, void** stream);
-/* Number of blocks a collective of this shape uses (identical on every rank);
- * kind: 0 all-reduce, 1 all-gather, 2 reduce-scatter, 3 broadcast, 4 reduce. */
+/* Number of blocks (lanes) a collective of this shape uses -- the per-collective
+ * grid size of PAPER.md:469, :488, identical on every rank; kind: 0 all-reduce,
+ * 1 all-gather, 2 reduce-scatter, 3 broadcast, 4 reduce.  Errors: occlInvalidArgument. */
 occlResult_t occlCollBlocks(occlComm_t comm, int kind, size_t count, occlDataType_t datatype,
                             int* nblocks);
 
