@@ -52,11 +52,12 @@ def intervals(tr):
 
 
 def coverage(ivs_by_rank, t_lo, t_hi, pair=False):
-    """Time during which all ranks (or rank r and r-1) run the same collective."""
+    """Time during which all ranks (or rank r and r-1) run the same collective, and
+    the start of the first all-rank alignment (None if never)."""
     n = len(ivs_by_rank)
     edges = sorted({t for ivs in ivs_by_rank for (a, b, _) in ivs for t in (a, b)} | {t_lo, t_hi})
     idx = [0] * n
-    aligned, paired = 0, 0
+    aligned, paired, first = 0, 0, None
     for k in range(len(edges) - 1):
         a, b = edges[k], edges[k + 1]
         mid = (a + b) / 2
@@ -69,8 +70,10 @@ def coverage(ivs_by_rank, t_lo, t_hi, pair=False):
             cur.append(ivs[i][2] if i < len(ivs) and ivs[i][0] <= mid < ivs[i][1] else None)
         if cur[0] is not None and all(c == cur[0] for c in cur):
             aligned += b - a
+            if first is None:
+                first = a
         paired += (b - a) * sum(1 for r in range(n) if cur[r] is not None and cur[r] == cur[r - 1]) / n
-    return aligned, paired
+    return aligned, paired, first
 
 
 def predicted_intersection(orders, lanes_of):
@@ -117,6 +120,7 @@ def run(policy, stick, order_kind, seed, args):
         blocks = {}
         nblocks = {c.coll_id: coll_blocks(c, n, G, int(comms[0].cfg.minBlockBytes)) for c in colls}
         q_first, q_pred, aligned_f, pair_f, runs_per_slice, run_len = [], [], [], [], [], []
+        q_align, t_align = [], []
         for b in range(0, G, max(1, G // args.sample_blocks)):
             trs = [comms[r].trace(b) for r in range(n)]
             if not all(trs):
@@ -124,7 +128,15 @@ def run(policy, stick, order_kind, seed, args):
             t_lo = min(tr[0][0] for tr in trs)
             t_hi = max(tr[-1][0] for tr in trs)
             ivs = [intervals(tr) for tr in trs]
-            al, pa = coverage(ivs, t_lo, t_hi)
+            al, pa, t_first = coverage(ivs, t_lo, t_hi)
+            if t_first is not None:
+                # queue length (admitted, not completed) of every rank's block b at the
+                # first moment all ranks ran the same collective
+                for r in range(n):
+                    f = sum(1 for t, ev, c, a in trs[r] if ev == "fetch" and t <= t_first)
+                    d = sum(1 for t, ev, c, a in trs[r] if ev == "done" and t <= t_first)
+                    q_align.append(f - d)
+                t_align.append((t_first - t_lo) / 1e3)
             aligned_f.append(al / max(1, t_hi - t_lo))
             pair_f.append(pa / max(1, t_hi - t_lo))
             for r in range(n):
@@ -149,6 +161,8 @@ def run(policy, stick, order_kind, seed, args):
         res = {"policy": ["fifo", "priority"][policy], "stickiness": stick, "order": order_kind, "seed": seed,
                "ms": ms, "preemptions": pre,
                "qlen_at_first_progress_median": statistics.median(q_first) if q_first else None,
+               "qlen_at_first_alignment_median": statistics.median(q_align) if q_align else None,
+               "us_to_first_alignment_median": statistics.median(t_align) if t_align else None,
                "qlen_predicted_intersection_median": statistics.median([q for q in q_pred if q]) if any(q_pred) else None,
                "aligned_frac_median": float(np.median(aligned_f)) if aligned_f else None,
                "pair_frac_median": float(np.median(pair_f)) if pair_f else None,
