@@ -74,6 +74,7 @@ def parse():
     ap.add_argument("--bulk-stores", type=int, default=0)
     ap.add_argument("--direct-read", type=int, default=1)
     ap.add_argument("--order-policy", type=int, default=1)
+    ap.add_argument("--force-sys", type=int, default=0, help="1: the headline ring on the connector-only / .sys path")
     ap.add_argument("--sq-yield-ns", type=int, default=-1, help="-1: library default")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -242,7 +243,7 @@ def bench_cfg(args, **extra):
               prefetchSlices=args.prefetch, discardConsumed=args.discard, l2Hints=args.l2_hints,
               directMode=args.direct, stagingTiles=args.stages, blocksPerSM=args.blocks_per_sm,
               bulkStores=args.bulk_stores, directRead=args.direct_read, maxColl=128, autoLaunch=0,
-              orderPolicy=args.order_policy)
+              orderPolicy=args.order_policy, forceSysScope=args.force_sys)
     if args.sq_yield_ns >= 0:
         kw["sqYieldNs"] = args.sq_yield_ns
     kw.update(extra)

@@ -127,6 +127,11 @@ typedef struct {
   uint64_t sqYieldNs;     /* priority policy: a collective blocked on a peer for >= spinMin spins yields to
                              newly submitted SQEs; its rank polls the host SQ for them at most once per
                              sqYieldNs (0 = never: new SQEs are seen only between runs) */
+  int llSpeculate;        /* 1 = LL slices are handed to the data warps before their lines arrived: the
+                             warps poll the lines themselves (one L2 round trip per hop less); a slice
+                             whose lines do not come within the spin threshold is aborted and redone
+                             later (LL lines are idempotent to rewrite).  0 = the control lane polls the
+                             slice's last line first */
 } occlConfig_t;
 
 /* Aggregate counters (device counters summed over blocks/collectives). */

@@ -227,6 +227,7 @@ struct SliceDesc {
   int prim;
   int dtype;
   int op;              // reducing function (kSum / kProd / kMax / kMin)
+  uint32_t gen;        // LL speculation: the pipe's abort generation when the slice was issued
 };
 
 template <int DT> struct Elem;
@@ -495,6 +496,12 @@ struct Pipe {
   uint64_t sdone[kMaxDepth];     // compute warps -> publisher: slice moved (count = compute warps)
   uint64_t empty[kMaxDepth];     // publisher + producer + compute -> control: slice published, descriptor read
   TraceCtl tr;                   // event-trace slot counter of this block
+  // LL speculation (cfg.llSpeculate): the control thread raises abortGen to make
+  // data warps give up slices whose lines have not arrived; a warp that gave up
+  // sets fail[i] before its sdone arrive.  Only the control thread writes
+  // abortGen and clears fail[i] (after empty[i], before reusing the slot).
+  uint32_t abortGen;
+  uint32_t fail[kMaxDepth];
 };
 
 struct Smem {
@@ -950,6 +957,11 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   char* connOut = R.dataNext + cb * K * p.sliceBytes;
   const char* directIn = p.flagsLocal + cb * kFlagStride + kDirectOff;   // {peer recvbuff, subSeq}
   const bool dOut = R.directNext != 0 && !ll, dIn = R.directPrev != 0 && !ll;
+  // LL speculation: recv slices go to the data warps before their lines arrived
+  // (the warps poll the lines themselves); a run whose oldest issued slice does
+  // not complete within the spin threshold aborts its speculative slices
+  const bool spec = ll && p.llSpeculate != 0;
+  uint64_t specSince = 0;
   const bool dRead = p.directRead != 0;
   const bool keepOut = p.l2Hints >= 3;
   const char* srcIn = p.flagsLocal + cb * kFlagStride + kDirectOff + 16;  // {upstream sendbuff, subSeq}
@@ -998,6 +1010,27 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     }
     advance(dc, cp, spc, nsteps);
   };
+  // drain the pipe before leaving the run: every issued slice completes (its
+  // connectors were ready) -- except, with LL speculation, slices whose lines have
+  // not come: the abort makes their warps give up, and only the prefix of slices
+  // that completed before the first given-up one is committed
+  auto drain = [&]() {
+    if (spec) *reinterpret_cast<volatile uint32_t*>(&pipe.abortGen) = pipe.abortGen + 1;
+    bool failed = false;
+    while (committed != issued) {
+      const uint32_t slot = committed % D;
+      mbar_wait(&pipe.empty[slot], (committed / D) & 1);
+      if (spec) {
+        if (*reinterpret_cast<volatile uint32_t*>(&pipe.fail[slot])) failed = true;
+        pipe.fail[slot] = 0;
+      }
+      if (!failed) {
+        commit(slot);
+        ++nSlices;
+      }
+      ++committed;
+    }
+  };
   int run;
   for (;;) {
     // ---- slices the data warps moved and published: advance the committed cursor
@@ -1012,6 +1045,17 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
         if (T > p.spinCap) T = p.spinCap;
       }
       m.tq[sh.pos] &= 0xffffu;                            // progressed: not stalled
+      specSince = 0;
+    }
+    if (spec && committed != issued) {                    // speculative slices outstanding
+      const uint64_t now = globaltimer();
+      if (specSince == 0) {
+        specSince = now;
+      } else if (now - specSince > T * spinNs) {          // the upstream is not there: preempt
+        drain();
+        run = RUN_PREEMPT;
+        break;
+      }
     }
     if (di.loop >= nloops) {                              // everything issued
       if (committed != issued) continue;
@@ -1071,7 +1115,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     const bool needRecv = prim & A_RECV, needSend = prim & A_SEND;
     bool ok = true;
     const long long tp = clock64();
-    if (needRecv && (prim & A_LL)) {
+    if (needRecv && (prim & A_LL) && !spec) {
       // LL: the data carries its own flags -- the last line of the slice holds
       // the message sequence number once the upstream wrote it
       uint32_t f0, f1;
@@ -1127,12 +1171,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
         }
       }
       if (yieldSq || now - spinStart > T * spinNs) {     // two-phase blocking: preempt
-        while (committed != issued) {                    // drain the pipe
-          mbar_wait(&pipe.empty[committed % D], (committed / D) & 1);
-          commit(committed % D);
-          ++committed;
-          ++nSlices;
-        }
+        drain();
         run = RUN_PREEMPT;                                // the prepared descriptor is dropped
         break;
       }
@@ -1141,6 +1180,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     spinStart = 0;
     if (prim & A_DOUT) sd.cout = reinterpret_cast<char*>(peerRecv) + doutOff;
     if (prim & A_DREAD) sd.cin = reinterpret_cast<const char*>(peerSrc) + dreadOff;   // same layout as ours
+    sd.gen = pipe.abortGen;
     mbar_arrive(&pipe.full[issued % D]);
     trace_at(p, *m.tr, b, kEvIssue, sh.curId,
           (uint32_t)(di.nsent & 0x3fff) | ((uint32_t)(di.nrecv & 0x3fff) << 14) | ((uint32_t)(prim & 0xf) << 28));
@@ -1383,7 +1423,8 @@ __device__ __forceinline__ void consume_tile(const int prim, char* dst, char* co
 template <int DT, int OP>
 __device__ __forceinline__ void ll_slice(const int prim, const char* src, const char* cin, char* dst, char* cout,
                                          const int64_t nelem, const uint32_t inSeq, const uint32_t outSeq,
-                                         const int tid, const int nt) {
+                                         const int tid, const int nt, const volatile uint32_t* abortGen,
+                                         const uint32_t gen, bool& ok) {
   typedef typename Elem<DT>::T T;
   constexpr int PER = 8 / sizeof(T);                 // elements per line
   const bool recv = prim & A_RECV, reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
@@ -1397,10 +1438,14 @@ __device__ __forceinline__ void ll_slice(const int prim, const char* src, const 
     const int64_t e0 = l * PER;
     if (recv) {
       uint32_t x0, f0, x1, f1;
-      do {
+      for (uint32_t spin = 0;; ++spin) {
         asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(x0), "=r"(f0), "=r"(x1), "=r"(f1) : "l"(cin + 16 * l) : "memory");
-      } while (f0 != inSeq || f1 != inSeq);
+        if (f0 == inSeq && f1 == inSeq) break;
+        // speculative slice the control thread gave up on: leave it (redone later;
+        // every line is idempotent to rewrite -- same data, same sequence number)
+        if ((spin & 7) == 7 && *abortGen != gen) { ok = false; return; }
+      }
       pay.w[0] = x0;
       pay.w[1] = x1;
       if (reduce) {
@@ -1485,6 +1530,17 @@ __device__ __forceinline__ void tail_slice(const int prim, const char* src, cons
     }                                                                              \
   } while (0)
 
+// LL slices out of line: the 24 (dtype, op) instantiations of the abortable
+// line loop would otherwise raise compute_main's register pressure into spills
+// on the bandwidth (TMA) path.
+__device__ __noinline__ bool ll_dispatch(int prim, int dtype, int op, const char* src, const char* cin, char* dst,
+                                         char* cout, int64_t nelem, uint32_t inSeq, uint32_t outSeq, int ctid,
+                                         int cnt, const volatile uint32_t* abortGen, uint32_t gen) {
+  bool ok = true;
+  OCCL_DISPATCH(dtype, op, ll_slice, prim, src, cin, dst, cout, nelem, inSeq, outSeq, ctid, cnt, abortGen, gen, ok);
+  return ok;
+}
+
 __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pipe, Stage* stages, uint64_t* tfull,
                                           uint64_t* tempty, uint64_t* tred, const int ctid, const int cnt) {
   const uint32_t D = (uint32_t)p.pipeDepth, S = (uint32_t)p.stages;
@@ -1503,12 +1559,12 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
     // lane 0 reads the descriptor and broadcasts it: the warp's only reader of
     // ring[i] is then the lane that hands it back on empty[i] (direct ordering)
     int prim = 0, dtype = 0, op = 0;
-    uint32_t inSeq = 0, outSeq = 0;
+    uint32_t inSeq = 0, outSeq = 0, gen = 0;
     unsigned long long nel = 0, a0 = 0, a1 = 0, a2 = 0, a3 = 0;
     if (lane == 0) {
       const SliceDesc* dp = &pipe.ring[i];
       prim = dp->prim; dtype = dp->dtype; op = dp->op;
-      inSeq = (uint32_t)dp->creditVal; outSeq = (uint32_t)dp->headVal;
+      inSeq = (uint32_t)dp->creditVal; outSeq = (uint32_t)dp->headVal; gen = dp->gen;
       nel = (unsigned long long)dp->nelem;
       a0 = (uintptr_t)dp->src; a1 = (uintptr_t)dp->cin; a2 = (uintptr_t)dp->dst; a3 = (uintptr_t)dp->cout;
     }
@@ -1518,6 +1574,7 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
     op = __shfl_sync(0xffffffffu, op, 0);
     inSeq = __shfl_sync(0xffffffffu, inSeq, 0);
     outSeq = __shfl_sync(0xffffffffu, outSeq, 0);
+    gen = __shfl_sync(0xffffffffu, gen, 0);
     const int64_t nelem = (int64_t)__shfl_sync(0xffffffffu, nel, 0);
     const char* src = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, a0, 0));
     const char* cin = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, a1, 0));
@@ -1526,7 +1583,9 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
     const long long t1 = clock64();
     const int vb = tma_vec_bytes(dtype, nelem, src, dst, cout, cin);
     if (prim & A_LL) {
-      OCCL_DISPATCH(dtype, op, ll_slice, prim, src, cin, dst, cout, nelem, inSeq, outSeq, ctid, cnt);
+      const bool ok = ll_dispatch(prim, dtype, op, src, cin, dst, cout, nelem, inSeq, outSeq, ctid, cnt,
+                                  &pipe.abortGen, gen);
+      if (__any_sync(0xffffffffu, !ok) && lane == 0) atomicOr(&pipe.fail[i], 1u);   // before sdone's release
     } else if (!(prim & (A_COPY | A_SEND))) {
       // direct final receive: the data is already in place, nothing to move
     } else if (vb == 0) {                              // small or misaligned: register path
@@ -1603,6 +1662,8 @@ __device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& 
   const uint64_t pol = policy_evict_first();
   uint32_t cs = 0, cph = 0;                         // bulk mode: staging slot / phase (same walk as the producer)
   uint32_t j = 0;
+  bool poisoned = false;                            // LL speculation: abort generation not to publish
+  uint32_t poisonGen = 0;
   for (;;) {
     const uint32_t i = j % D;
     mbar_wait(&pipe.full[i], (j / D) & 1);
@@ -1648,6 +1709,17 @@ __device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& 
     }
     mbar_wait(&pipe.sdone[i], (j / D) & 1);
     if (bulkSlice) bulk_wait_all();                  // the slice's bulk writes are complete
+    {
+      // LL speculation: a slice a data warp gave up on -- and every later slice of
+      // the same abort generation -- is not published; the control thread redoes it
+      const uint32_t g = pipe.ring[i].gen;
+      if (*reinterpret_cast<volatile uint32_t*>(&pipe.fail[i])) { poisoned = true; poisonGen = g; }
+      if (poisoned && g == poisonGen) {
+        mbar_arrive(&pipe.empty[i]);
+        ++j;
+        continue;
+      }
+    }
     bool send = false, recv = false, needFence = false;
     uint64_t hv = 0, cv = 0;
     char* ho = nullptr;
@@ -1668,6 +1740,7 @@ __device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& 
       if ((d1.prim & A_SEND) && ho && d1.headOut != ho) break;
       if ((d1.prim & A_RECV) && co && d1.creditOut != co) break;
       if (!mbar_test(&pipe.sdone[k1 % D], (k1 / D) & 1)) break;
+      if (*reinterpret_cast<volatile uint32_t*>(&pipe.fail[k1 % D])) break;   // handled on its own
       k = k1;
     }
     trace_at(p, pipe.tr, b, kEvSdone, k - j + 1, (uint32_t)(hv & 0xffff) | ((uint32_t)(cv & 0xffff) << 16));
@@ -1746,6 +1819,8 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
     for (int w = 0; w < W; ++w) m.cacheTag[w] = -1;
     pipe.tr.base = p.traceCap ? p.traceCount[b] : 0;
     pipe.tr.idx = 0;
+    pipe.abortGen = 0;
+    for (int i = 0; i < kMaxDepth; ++i) pipe.fail[i] = 0;
     sh.lastFetch = globaltimer();
     for (uint32_t i = 0; i < D; ++i) {
       mbar_init(&pipe.full[i], 1);

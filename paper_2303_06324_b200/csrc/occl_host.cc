@@ -590,6 +590,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->blocksPerSM = 1;
   c->l2Hints = 2;
   c->sqYieldNs = 20'000;
+  c->llSpeculate = 0;
   return occlSuccess;
 }
 
@@ -835,6 +836,7 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   p.l2Hints = c->cfg.l2Hints;
   p.stallNs = c->cfg.stallNs;
   p.sqYieldNs = c->cfg.sqYieldNs;
+  p.llSpeculate = c->cfg.llSpeculate;
   Launcher* L = new Launcher();
   if ((r = launcher_start(L, {c})) != occlSuccess) {
     launcher_stop(L);

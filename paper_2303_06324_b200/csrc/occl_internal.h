@@ -230,6 +230,7 @@ struct DaemonParams {
   uint32_t quitTotal;               // blocks of the launch (G x fused members)
   uint64_t stallNs;                 // FIFO: all entries stuck when none progressed for this long (0: off)
   uint64_t sqYieldNs;               // priority: host-SQ poll period of blocked collectives (0: no yield)
+  int llSpeculate;                  // LL: issue recv slices before their lines arrived (abortable)
   // CQ variant (NEXT-3 ablation): 0 = id slots (cqDone, default),
   // 1 = vanilla MPSC ring (entry, fence, in-order tail update), 2 = packed 64-bit
   // ring entries {stamp, id} (one host write, no fence between entry and tail)

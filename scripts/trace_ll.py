@@ -1,0 +1,86 @@
+#!/usr/bin/env python
+"""Where a small (LL) all-reduce's hop goes, from the device trace: 8 virtual
+ranks, one collective of --bytes (default 4 KiB, LL protocol, one block), the
+daemon kept alive between samples.  Per hop (rank r step j+1 consuming rank
+r-1's step j):
+  detect  = issue(r, j+1) - sdone(r-1, j)   upstream's lines stored -> our control lane saw them
+  move    = sdone(r, j+1) - issue(r, j+1)   descriptor -> compute warps polled, reduced, stored
+and the per-collective split: first fetch -> first switch-in, switch-in -> done.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2303_06324_b200 import harness, occl  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--bytes", type=int, default=4096)
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--grid", type=int, default=18)
+    ap.add_argument("--ll-max", type=int, default=-1)
+    ap.add_argument("--ll-spec", type=int, default=0)
+    ap.add_argument("--out", default="gpurun_out/trace_ll.json")
+    a = ap.parse_args()
+    torch.cuda.set_device(0)
+    n = 8
+    extra = {"llMaxBytes": a.ll_max} if a.ll_max >= 0 else {}
+    if a.ll_spec:
+        extra["llSpeculate"] = 1
+    comms = harness.ring(n, 0, gridBlocks=a.grid, maxColl=16, traceCap=1 << 14, quitIdleNs=10_000_000_000, **extra)
+    cid = 1
+    count = a.bytes // 4
+    bufs = harness.buffers("allreduce", "f32", n, count, comms)
+    det, mov, exe, adm = [], [], [], []
+    try:
+        for rep in range(a.reps):
+            for c in comms:
+                c.submit("allreduce", bufs[comms.index(c)][0], bufs[comms.index(c)][1], cid, count, "f32")
+            for c in comms:
+                c.wait(cid, 60)
+            if rep < 3:
+                continue
+            b = cid % a.grid
+            tr = [comms[r].trace(b) for r in range(n)]
+            # this repetition's events only: after the last "fetch" of cid on each rank
+            evs = []
+            for r in range(n):
+                f = max(i for i, (t, e, c, x) in enumerate(tr[r]) if e == "fetch" and c == cid)
+                evs.append(tr[r][f:])
+            issue = [[t for t, e, c, x in ev if e == "issue" and c == cid] for ev in evs]
+            sdone = [[t for t, e, c, x in ev if e == "sdone"] for ev in evs]
+            for r in range(n):
+                up = (r - 1) % n
+                for j in range(1, min(len(issue[r]), len(sdone[up]) + 1)):
+                    if j < len(issue[r]) and j - 1 < len(sdone[up]):
+                        det.append((issue[r][j] - sdone[up][j - 1]) / 1e3)
+                for j in range(min(len(issue[r]), len(sdone[r]))):
+                    mov.append((sdone[r][j] - issue[r][j]) / 1e3)
+                sw = [t for t, e, c, x in evs[r] if e == "switch_in" and c == cid]
+                dn = [t for t, e, c, x in evs[r] if e == "done" and c == cid]
+                if sw and dn:
+                    exe.append((dn[-1] - sw[0]) / 1e3)
+                    adm.append((sw[0] - evs[r][0][0]) / 1e3)
+        res = {"bytes": a.bytes, "hops_sampled": len(det),
+               "detect_us_median": statistics.median(det) if det else None,
+               "detect_us_p10": sorted(det)[len(det) // 10] if det else None,
+               "move_us_median": statistics.median(mov) if mov else None,
+               "execute_us_median": statistics.median(exe) if exe else None,
+               "fetch_to_switchin_us_median": statistics.median(adm) if adm else None,
+               "issues_per_rank": len(issue[0])}
+        print(json.dumps(res))
+        with open(a.out, "w") as f:
+            json.dump(res, f)
+    finally:
+        occl.destroy_group(comms)
+
+
+if __name__ == "__main__":
+    main()

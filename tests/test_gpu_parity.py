@@ -59,11 +59,14 @@ def test_generator_matches_numpy(occl_mod):
 @pytest.mark.parametrize("kind", ring.KINDS)
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
-@pytest.mark.parametrize("proto", ["ll", "simple"])
+@pytest.mark.parametrize("proto", ["ll", "ll-spec", "simple"])
 def test_parity_small(occl_mod, kind, dtype, n, proto):
-    """LL (flags inside 16-B lines) for small per-block parts, Simple (head /
-    credit flags + release fence) when LL is disabled."""
-    comms = group(occl_mod, n, llMaxBytes=(64 << 10) if proto == "ll" else 0)
+    """LL (flags inside 16-B lines) for small per-block parts -- with the data
+    warps polling the lines themselves (ll-spec, cfg.llSpeculate) or after the
+    control lane saw the slice's last line -- and Simple (head / credit flags +
+    release fence) when LL is disabled."""
+    comms = group(occl_mod, n, llMaxBytes=0 if proto == "simple" else (64 << 10),
+                  llSpeculate=int(proto == "ll-spec"))
     for ci, count in enumerate([1, 7, 256, 1000, 4099, 65536]):
         root = (ci + 1) % n
         seed = 1000 + ci
@@ -85,11 +88,12 @@ def test_parity_inplace(occl_mod, kind, n):
 
 
 @pytest.mark.parametrize("n", [2, 4, 8])
-@pytest.mark.parametrize("llmax", [0, 1 << 20])
-def test_parity_1mib_multiblock(occl_mod, n, llmax):
+@pytest.mark.parametrize("llmax,spec", [(0, 0), (1 << 20, 0), (1 << 20, 1)])
+def test_parity_1mib_multiblock(occl_mod, n, llmax, spec):
     """1 Mi elements: many loops and slices per block, ragged tail, all blocks;
-    Simple, and LL forced for every size (many LL slices and loops)."""
-    comms = group(occl_mod, n, llMaxBytes=llmax)
+    Simple, and LL forced for every size (many LL slices and loops), with and
+    without LL speculation."""
+    comms = group(occl_mod, n, llMaxBytes=llmax, llSpeculate=spec)
     for kind in ring.KINDS:
         count = (1 << 20) + 13
         sends, recvs = U.make_bufs(kind, "f32", n, count, 5, 3)

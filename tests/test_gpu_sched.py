@@ -83,6 +83,29 @@ def test_random_orders_forced_preemption(occl_mod, T):
         occl_mod.destroy_group(comms)
 
 
+@pytest.mark.parametrize("T", [1, 8, 4096])
+def test_ll_speculation_random_orders(occl_mod, T):
+    """LL speculation (cfg.llSpeculate): recv slices are handed to the data warps
+    before their lines arrived; under misordered submissions and tiny thresholds
+    the control thread aborts them and redoes them later.  Every collective here
+    is LL-sized; results must stay bit-exact and, at T = 1, aborts must happen."""
+    comms = occl_mod.local_group(8, 0, **BASE, llSpeculate=1, spinBase=T, spinStep=1, spinMin=1,
+                                 spinCap=max(T, 4 * T))
+    try:
+        rng = random.Random(1000 + T)
+        kinds = ["allreduce", "allgather", "reducescatter", "broadcast"]
+        colls = [workloads.Coll(i, kinds[i % 4], ["f32", "bf16", "i32"][i % 3], rng.randint(1, 6_000),
+                                root=rng.randrange(8)) for i in range(8)]
+        for it in range(4):
+            orders = [rng.sample(range(8), 8) for _ in range(8)]
+            _run_orders(comms, colls, orders, seed=300 * T + it)
+        pre = sum(c.stats()["preemptions"] for c in comms)
+        if T == 1:
+            assert pre > 0
+    finally:
+        occl_mod.destroy_group(comms)
+
+
 def test_deadlock_campaign_small(occl_mod):
     """PAPER.md:736-739 at n=8: ARs of 256 B..1 MiB in independent random per-rank
     orders; every trial must complete (0 timeouts) and match the oracle."""
