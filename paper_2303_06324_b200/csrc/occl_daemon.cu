@@ -792,8 +792,21 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
     bool fetched = false;
     uint64_t tail = ld_acquire(p.mirrorTail, 0);
     if (tail <= sh.cursor) {
-      sq_fetch(p, m, b);                             // one block at a time copies host SQEs to the mirror
-      tail = ld_acquire(p.mirrorTail, 0);
+      // The host SQ itself (a PCIe round trip under the rank's fetch lock) is
+      // polled at once by an idle block, but by a block with queued work at most
+      // once per sqYieldNs per rank: otherwise a block about to run a collective
+      // it just admitted would first wait for a PCIe round trip.  (sqYieldNs = 0:
+      // no rate limit.)  Liveness: some block of the rank polls within sqYieldNs.
+      bool poll = qlen == 0 || p.sqYieldNs == 0;
+      if (!poll) {
+        unsigned long long* lastHost = reinterpret_cast<unsigned long long*>(p.mirrorTail + 3);
+        const unsigned long long lh = *reinterpret_cast<volatile unsigned long long*>(lastHost);
+        poll = now - lh > p.sqYieldNs && atomicCAS(lastHost, lh, (unsigned long long)now) == lh;
+      }
+      if (poll) {
+        sq_fetch(p, m, b);                           // one block at a time copies host SQEs to the mirror
+        tail = ld_acquire(p.mirrorTail, 0);
+      }
     }
     for (int k = 0; k < burst && !sh.exiting && sh.qlen < (uint32_t)p.maxColl && sh.cursor < tail; ++k) {
       // the SQE from the device-memory mirror (L2), 4 independent 16-B loads
