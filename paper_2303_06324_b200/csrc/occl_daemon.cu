@@ -594,8 +594,17 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched
     if (p.sysScope) asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(f + 8), "l"(e.subSeq) : "memory");
     else asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(f + 8), "l"(e.subSeq) : "memory");
   }
+  // install the fresh context in its cache way as well: the collective just
+  // admitted usually runs next, and this saves its first context load (a global
+  // round trip).  Every cached context is clean between runs (a run's end saves
+  // it), so evicting the way's occupant loses nothing.
   const int way = c % W;
-  if (m.cacheTag[way] == c) m.cacheTag[way] = -1;
+  {
+    uint4* cw = reinterpret_cast<uint4*>(&m.cache[way]);
+#pragma unroll
+    for (int i = 0; i < kCtxBytes / 16; ++i) cw[i] = w[i];
+    m.cacheTag[way] = c;
+  }
   m.prio[c] = e.priority;
   if (p.orderPolicy == 0) {
     m.tq[sh.qlen++] = (uint32_t)c;                  // FIFO: tail
@@ -627,6 +636,8 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched
 __device__ __noinline__ bool sq_fetch(const DaemonParams& p, const Smem& m, Sched& sh, int b) {
   if (atomicCAS(p.fetchLock, 0u, 1u) != 0u) return true;       // another block is fetching
   trace_at(p, *m.tr, b, kEvMark, 0, 1);
+  // any host poll restarts the rank's rate-limit clock for busy blocks (schedule())
+  *reinterpret_cast<volatile unsigned long long*>(p.mirrorTail + 3) = (unsigned long long)globaltimer();
   uint64_t t = ld_relaxed(p.mirrorTail, 0);
   // the slowest block's cursor bounds which mirror slots may be overwritten; a
   // cached value is a safe lower bound (cursors only grow), so the G cursors are

@@ -35,12 +35,19 @@ def main():
     colls, _ = workloads.c4("resnet50", n, 0, per_tensor=True)
     order = list(range(len(colls)))[::-1]               # backward pass: last layer first
     rows = []
-    for policy, stick in ((0, 1), (0, 0), (1, 1)):
+    # (policy, stickiness, priority rule): the priority policy with its default
+    # priority = collId, and with a user-defined priority = position in the
+    # backward-pass submission order (occlSetPriority, globally agreed)
+    for policy, stick, prio in ((0, 1, "-"), (0, 0, "-"), (1, 1, "collId"), (1, 1, "submission")):
         comms = harness.ring(n, 0, gridBlocks=16, maxColl=256, autoLaunch=0, orderPolicy=policy,
                              stickiness=stick, traceCap=1 << 15, spinBase=args.spin_base,
                              spinStep=max(1, args.spin_base // 8), spinMin=min(128, args.spin_base),
                              spinCap=args.spin_cap)
         bufs = {c.coll_id: harness.buffers(c.kind, c.dtype, n, c.count, comms) for c in colls}
+        if prio == "submission":
+            for pos, k in enumerate(order):
+                for c in comms:
+                    c.set_priority(colls[k].coll_id, pos)
         torch.cuda.synchronize()
         for c in comms:
             c.trace_reset()
@@ -78,7 +85,7 @@ def main():
         tr = comms[1].trace(0)
         sw = [a for t, ev, c, a in tr if ev == "switch_in"]
         pre = sum(1 for t, ev, c, a in tr if ev == "preempt")
-        row = {"policy": ["fifo", "priority"][policy], "stickiness": stick, "delay_ms": args.delay_ms,
+        row = {"policy": ["fifo", "priority"][policy], "stickiness": stick, "priority": prio, "delay_ms": args.delay_ms,
                "spin_base": args.spin_base, "spin_cap": args.spin_cap,
                "makespan_ms": ms, "after_straggler_ms": ms - args.delay_ms, **d,
                "rank1_block0": {"switch_ins": len(sw), "preemptions": pre,
