@@ -486,6 +486,7 @@ struct Sched {
   uint64_t lastProgress;       // %globaltimer of the last run that committed a slice
   uint64_t lastSqPoll;         // %globaltimer of this block's last SQ check while blocked (priority policy)
   uint32_t sqPhase;            // parity of the SQ staging mbarrier
+  uint32_t needHostPoll;       // a blocked run yielded because the host SQ holds a new SQE
   int lastRun, curId;
   int way;
   unsigned long long cycRun, cycPoll, cycAcqFence, cycRelFence, nCommit;   // probes
@@ -817,13 +818,14 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
       // once per sqYieldNs per rank: otherwise a block about to run a collective
       // it just admitted would first wait for a PCIe round trip.  (sqYieldNs = 0:
       // no rate limit.)  Liveness: some block of the rank polls within sqYieldNs.
-      bool poll = qlen == 0 || p.sqYieldNs == 0;
+      bool poll = qlen == 0 || p.sqYieldNs == 0 || sh.needHostPoll;
       if (!poll) {
         unsigned long long* lastHost = reinterpret_cast<unsigned long long*>(p.mirrorTail + 3);
         const unsigned long long lh = *reinterpret_cast<volatile unsigned long long*>(lastHost);
         poll = now - lh > p.sqYieldNs && atomicCAS(lastHost, lh, (unsigned long long)now) == lh;
       }
       if (poll) {
+        sh.needHostPoll = 0;
         sq_fetch(p, m, sh, b);                           // one block at a time copies host SQEs to the mirror
         tail = ld_acquire(p.mirrorTail, 0);
       }
@@ -1200,6 +1202,9 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
             asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(stamp) : "l"(p.sq[tail % p.sqDepth].c[0])
                          : "memory");
             yieldSq = stamp == (uint32_t)(tail + 1);
+            // the scheduler must fetch it now: its own host polls are rate
+            // limited by the clock this peek just restarted
+            if (yieldSq) sh.needHostPoll = 1;
           }
         }
       }
@@ -1835,6 +1840,7 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
     sh.lastProgress = 0;
     sh.lastSqPoll = 0;
     sh.sqPhase = 0;
+    sh.needHostPoll = 0;
     mbar_init(&sqbar, 1);
     sh.lastRun = -1;
     sh.curId = -1;

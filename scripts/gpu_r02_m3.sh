@@ -7,4 +7,5 @@ for spec in 0 1; do for b in 4096 65536; do
 done; done
 timeout 900 python scripts/latency_split.py --kinds allreduce --ll-spec 1 --tag llspec --out gpurun_out/m3_lat_llspec > gpurun_out/m3_lat_llspec.log 2>&1; echo "lat llspec rc=$?"
 bash scripts/gpu_variants.sh scripts/var_r02c.txt vc 2 0
+timeout 120 python scripts/probe_multicast.py > gpurun_out/m3_multicast.json 2>&1; echo "probe rc=$?"; tail -c 1500 gpurun_out/m3_multicast.json
 timeout 900 python scripts/fifo_diagnosis.py --seeds 1 --out gpurun_out/m3_fifo_diag.jsonl > gpurun_out/m3_fifo_diag.log 2>&1; echo "fifo diag rc=$?"; cut -c1-500 gpurun_out/m3_fifo_diag.log | tail -4
