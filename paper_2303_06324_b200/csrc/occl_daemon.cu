@@ -917,8 +917,14 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
       p.collStats[(size_t)c * G + b].ctxLoads++;
     }
     sh.curId = c;
-    // initial spin threshold from the queue position
-    if (p.stickiness) {
+    // initial spin threshold from the queue position.  Under
+    // the priority policy (reading R10) the front is where every rank converges;
+    // a lower-priority entry is visited only for as long as it progresses
+    // (spinMin of waiting), so a rank does not hold a peer-less entry while the
+    // others arrive at the front
+    if (p.stickiness && p.orderPolicy == 1 && sh.pos != 0) {
+      sh.T = p.spinMin;
+    } else if (p.stickiness) {
       const uint64_t dec = (uint64_t)sh.pos * p.spinStep;
       uint64_t T = dec >= p.spinBase ? p.spinMin : p.spinBase - dec;
       sh.T = T < p.spinMin ? p.spinMin : T;
@@ -1075,7 +1081,12 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
         ++committed;
         ++nSlices;
       } while (committed != issued && mbar_test(&pipe.empty[committed % D], (committed / D) & 1));
-      if (p.stickiness) {                                 // raise the threshold
+      // raise the threshold.  Priority policy (reading R10): only
+      // the queue front -- the collective every rank converges on -- is boosted;
+      // a visit to a lower-priority entry keeps its short position threshold, so
+      // progress a pair of neighbours makes on it (up to K slices) does not make
+      // a rank stick to it for up to spinCap while the others wait at the front
+      if (p.stickiness && !(p.orderPolicy == 1 && sh.pos != 0)) {
         T *= p.spinBoost;
         if (T > p.spinCap) T = p.spinCap;
       }
