@@ -136,6 +136,7 @@ def live_run(comms, jobs, orders, delays, iterations=1, timeout_s=300.0, orders_
         c.set_auto_launch(True)
     bar = threading.Barrier(n + 1)
     first = [[None] * iterations for _ in range(n)]
+    sub_t = [[dict() for _ in range(iterations)] for _ in range(n)]   # [rank][it][job index] -> submit time
     last = [[None] * iterations for _ in range(n)]
     errors = []
 
@@ -156,6 +157,7 @@ def live_run(comms, jobs, orders, delays, iterations=1, timeout_s=300.0, orders_
                     s, r = bufs[li]
                     if first[li][it] is None:
                         first[li][it] = time.perf_counter()
+                    sub_t[li][it][k] = time.perf_counter()
                     c.submit(kind, s, r, cid, count, dtype, root)
                 for k in od:
                     c.wait(jobs[k][0], timeout_s)
@@ -180,4 +182,8 @@ def live_run(comms, jobs, orders, delays, iterations=1, timeout_s=300.0, orders_
     iter_ms = [(max(last[r][it] for r in range(n)) - min(first[r][it] for r in range(n))) * 1e3
                for it in range(iterations)]
     makespan = (max(last[r][-1] for r in range(n)) - min(first[r][0] for r in range(n))) * 1e3
-    return {"makespan_ms": makespan, "iter_ms": iter_ms}
+    # per iteration and job: when the LAST rank submitted it (a collective cannot
+    # start earlier), relative to the iteration's first submission, in ms
+    ready_ms = [{k: (max(sub_t[r][it][k] for r in range(n)) - min(first[r][it] for r in range(n))) * 1e3
+                 for k in sub_t[0][it]} for it in range(iterations)]
+    return {"makespan_ms": makespan, "iter_ms": iter_ms, "ready_ms": ready_ms}

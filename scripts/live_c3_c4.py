@@ -13,8 +13,13 @@ of gradient buckets, ids resubmitted each step.  mean gap = one collective's
 time (measured: consistent no-jitter makespan / #collectives).
 
 Reported per row: makespan (C3) or median iteration time (C4), preemption
-counts, and overhead = T_random / T_consistent - 1.  A summary per (workload,
-variant) gives the median and min-max over seeds x repeats.
+counts, overhead = T_random / T_consistent - 1, and -- because a collective
+cannot start before its LAST rank submitted it, which under independent random
+orders is late in the submission window whatever the scheduler does -- the
+overhead against the ideal gang-scheduled makespan for the SAME arrivals
+(ideal_ms: the collectives back to back in the order they became ready, each
+at its standalone device time; DESIGN.md §5 "live arrival").  A summary per
+(workload, variant) gives the median and min-max over seeds x repeats.
 """
 import argparse
 import json
@@ -52,6 +57,28 @@ def stats_delta(comms, before):
                                                                         "launches", "cqeWritten")}
 
 
+def ideal_ms(ready, dur):
+    """Ideal gang-scheduled makespan given the arrivals: the collectives run one
+    after another, each as soon as every rank submitted it (ready[k], ms after the
+    iteration's first submission) and the previous one finished, each taking its
+    standalone device time dur[k] -- what a scheduler with perfect knowledge of
+    the arrivals achieves without preemption cost (collectives using fewer blocks
+    could overlap, so this is a reference, not a strict bound)."""
+    t = 0.0
+    for k in sorted(ready, key=lambda j: ready[j]):
+        t = max(t, ready[k]) + dur[k]
+    return t
+
+
+def standalone_ms(comms, jobs):
+    """Device time of each collective alone (one daemon launch each, median of 3)."""
+    out = {}
+    for k, job in enumerate(jobs):
+        ts = sorted(harness.timed_batch(comms, [job]) for _ in range(3))
+        out[k] = ts[1]
+    return out
+
+
 def one(comms, jobs, n, ncoll, iters, seed, rep, mean_gap, order_kind):
     base = seed * 7919 + rep * 104729 + (0 if order_kind == "consistent" else 1)
     if order_kind == "consistent":
@@ -64,6 +91,11 @@ def one(comms, jobs, n, ncoll, iters, seed, rep, mean_gap, order_kind):
     st = stats_delta(comms, before)
     t = r["makespan_ms"] if iters == 1 else statistics.median(r["iter_ms"])
     return t, st, r
+
+
+def ideal_of(r, dur, iters):
+    v = [ideal_ms(rd, dur) for rd in r["ready_ms"]]
+    return v[0] if iters == 1 else statistics.median(v)
 
 
 def main():
@@ -114,16 +146,23 @@ def main():
                 iters = 1 if wname == "c3" else (args.fifo_iterations if fifo else args.iterations)
                 bufs = {c.coll_id: harness.buffers(c.kind, c.dtype, n, c.count, comms) for c in colls}
                 jobs = [(c.coll_id, c.kind, c.dtype, c.count, c.root, bufs[c.coll_id]) for c in colls]
+                dur = standalone_ms(comms, jobs)
+                for c in comms:
+                    c.set_auto_launch(True)
                 # calibration: consistent order, no jitter (also first touch of buffers / arena)
                 t_cal, _, _ = one(comms, jobs, n, ncoll, 1, seed, 99, 0.0, "consistent")
                 t_cal, _, _ = one(comms, jobs, n, ncoll, 1, seed, 98, 0.0, "consistent")
                 mean_gap = t_cal / 1e3 / ncoll
                 for rep in range(args.repeats):
-                    tc, sc, _ = one(comms, jobs, n, ncoll, iters, seed, rep, mean_gap, "consistent")
+                    tc, sc, rc = one(comms, jobs, n, ncoll, iters, seed, rep, mean_gap, "consistent")
                     tr, sr, rr = one(comms, jobs, n, ncoll, iters, seed, rep, mean_gap, "random")
+                    ic, ir = ideal_of(rc, dur, iters), ideal_of(rr, dur, iters)
                     row = {"tag": args.tag, "knobs": extra, "workload": wname, "variant": vname, "seed": seed, "repeat": rep, "ranks": n,
                            "ncoll": ncoll, "iterations": iters, "mean_gap_us": mean_gap * 1e6,
                            "ms_consistent": tc, "ms_random": tr, "overhead": tr / tc - 1.0,
+                           "ideal_ms_consistent": ic, "ideal_ms_random": ir,
+                           "overhead_vs_ideal_consistent": tc / ic - 1.0, "overhead_vs_ideal_random": tr / ir - 1.0,
+                           "standalone_ms_total": sum(dur.values()),
                            "preempt_consistent": sc["preemptions"], "preempt_random": sr["preemptions"],
                            "launches_random": sr["launches"], "quits_random": sr["quits"],
                            "iter_ms_random_p90": (sorted(rr["iter_ms"])[int(0.9 * (len(rr["iter_ms"]) - 1))]
@@ -147,6 +186,9 @@ def main():
                          "ms_consistent_median": statistics.median(r["ms_consistent"] for r in rs),
                          "ms_random_median": statistics.median(r["ms_random"] for r in rs),
                          "overhead_median": statistics.median(ov), "overhead_min": ov[0], "overhead_max": ov[-1],
+                         "overhead_vs_ideal_random_median": statistics.median(r["overhead_vs_ideal_random"] for r in rs),
+                         "overhead_vs_ideal_consistent_median": statistics.median(r["overhead_vs_ideal_consistent"]
+                                                                                  for r in rs),
                          "preempt_random_median": statistics.median(r["preempt_random"] for r in rs),
                          "preempt_consistent_median": statistics.median(r["preempt_consistent"] for r in rs)})
     with open(args.out + "_summary.json", "w") as f:
