@@ -33,7 +33,7 @@ def test_bench_multiprocess_path():
     env = dict(os.environ, OCCL_BENCH_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"), "--gpus", "2",
-           "--size-mib", "8", "--sizes", "2,8", "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu", "--check"]
+           "--size-mib", "8", "--sizes", "2,8", "--steps", "3", "--warmup", "3", "--no-cpu", "--check"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=400, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
@@ -45,3 +45,5 @@ def test_bench_multiprocess_path():
     assert head["check"]["bit_exact"] and len(d["sweep"]) == 2
     assert d["roofline"]["bound"] == "nvlink" and d["scaling"] == "weak"
     assert "unavailable" in d["baseline"]["nccl"]                 # gloo plumbing on one GPU: no NCCL arm
+    # end to end through the public API: H2D + occlAllReduce + occlWait + D2H per step
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 8 << 20
