@@ -408,9 +408,20 @@ int coll_blocks(const occlComm* c, int kind, size_t count, int dtype) {
     seg = (per + A - 1) / A * A;
   }
   const uint64_t bytes = seg * isz;
+  const uint64_t G = (uint64_t)c->cfg.gridBlocks;
   uint64_t nb = (bytes + c->cfg.minBlockBytes - 1) / c->cfg.minBlockBytes;
   if (nb < 1) nb = 1;
-  if (nb > (uint64_t)c->cfg.gridBlocks) nb = c->cfg.gridBlocks;
+  if (nb > G) nb = G;
+  // Latency-bound collectives (the whole segment fits in one LL slice per block
+  // of the grid): spread them so every block moves ONE LL slice per step.  A
+  // ring step then costs one LL hop (~3 us at 8 ranks) whatever the size, where
+  // a single block would chain several slices per step (a 256 KiB all-reduce at
+  // 8 ranks: 4 slices x 14 steps on one block, slower than 1 MiB on Simple).
+  // Same on every rank: a function of (count, dtype, nranks, config).
+  if (c->cfg.llMaxBytes && c->nranks > 1 && bytes <= G * (uint64_t)c->cfg.llSliceBytes) {
+    uint64_t nbLL = (bytes + c->cfg.llSliceBytes - 1) / c->cfg.llSliceBytes;
+    if (nbLL > nb) nb = nbLL;
+  }
   return (int)nb;
 }
 

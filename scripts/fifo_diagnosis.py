@@ -91,16 +91,6 @@ def predicted_intersection(orders, lanes_of):
     return None
 
 
-def coll_blocks(c, n, G, min_block_bytes):
-    """Blocks a collective uses (the host's rule: ceil(segment bytes / minBlockBytes), <= G)."""
-    isz = harness.ITEM[c.dtype]
-    seg = c.count
-    if n > 1 and c.kind == "allreduce":
-        a = 16 // isz
-        seg = ((c.count + n - 1) // n + a - 1) // a * a
-    return max(1, min(G, -(-seg * isz // min_block_bytes)))
-
-
 def run(policy, stick, order_kind, seed, args):
     n, G = 8, args.grid
     comms = harness.ring(n, 0, gridBlocks=G, maxColl=256, autoLaunch=0, orderPolicy=policy, stickiness=stick,
@@ -118,7 +108,7 @@ def run(policy, stick, order_kind, seed, args):
         ms = harness.timed_batch(comms, jobs, orders, timeout_s=600)
         pre = sum(c.stats()["preemptions"] - b["preemptions"] for c, b in zip(comms, before))
         blocks = {}
-        nblocks = {c.coll_id: coll_blocks(c, n, G, int(comms[0].cfg.minBlockBytes)) for c in colls}
+        nblocks = {c.coll_id: comms[0].coll_blocks(c.kind, c.count, c.dtype) for c in colls}   # occlCollBlocks
         q_first, q_pred, aligned_f, pair_f, runs_per_slice, run_len = [], [], [], [], [], []
         q_align, t_align = [], []
         for b in range(0, G, max(1, G // args.sample_blocks)):
