@@ -475,6 +475,8 @@ constexpr int kTmaMinBytes = 16384;    // slices below this use register loads (
 constexpr uint32_t kQuitLatch = 0x80000000u;   // quitWord: every block of the launch voted to quit
 constexpr uint64_t kSqPollNs = 2000;           // a blocked collective polls the SQ at most this often
 constexpr int kSqBurst = 4;                    // host SQ slots read by one bulk copy
+constexpr int kBoardOff = kDirectOff + 64;     // readiness board slot in the (collId, block 0) direct line
+constexpr int kReadyScan = 8;                  // queue entries the priority scheduler checks for readiness
 
 // Scheduler state of one block; touched only by the control thread.
 struct Sched {
@@ -487,6 +489,7 @@ struct Sched {
   uint64_t lastSqPoll;         // %globaltimer of this block's last SQ check while blocked (priority policy)
   uint32_t sqPhase;            // parity of the SQ staging mbarrier
   uint32_t needHostPoll;       // a blocked run yielded because the host SQ holds a new SQE
+  uint32_t boostOk;            // the running entry may be boosted (stickiness, R10 / R29)
   int lastRun, curId;
   int way;
   unsigned long long cycRun, cycPoll, cycAcqFence, cycRelFence, nCommit;   // probes
@@ -523,6 +526,9 @@ struct Smem {
   int* cacheTag;       // [W]
   uint32_t* tq;        // [maxColl] task queue: id | stall << 16
   int32_t* prio;       // [maxColl] priority of each queued collective (by id)
+  uint32_t* subLo;     // [maxColl] low 32 bits of each queued collective's submission number
+  uint8_t* subOf;      // [maxColl] its ring (RingDesc index)
+  uint8_t* ready;      // [maxColl] every member admitted it (readiness board, reading R29)
   SqeWire* sqbuf;      // [kSqBurst] host SQ slots read by one TMA bulk copy (sq_fetch)
   uint64_t* sqbar;     // its mbarrier
 };
@@ -607,6 +613,15 @@ __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched
     m.cacheTag[way] = c;
   }
   m.prio[c] = e.priority;
+  m.subLo[c] = (uint32_t)e.subSeq;
+  m.subOf[c] = (uint8_t)e.sub;
+  m.ready[c] = (n == 1) ? 1 : 0;
+  if (lane == 0 && p.orderPolicy == 1 && p.readyFirst) {
+    // readiness board (reading R29): this rank admitted submission subSeq of c
+    char* slot = p.flagsLocal + (size_t)c * G * kFlagStride + kBoardOff;
+    if (p.sysScope) asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(slot), "l"(e.subSeq) : "memory");
+    else asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(slot), "l"(e.subSeq) : "memory");
+  }
   if (p.orderPolicy == 0) {
     m.tq[sh.qlen++] = (uint32_t)c;                  // FIFO: tail
   } else {
@@ -709,6 +724,24 @@ __device__ __noinline__ bool sq_fetch(const DaemonParams& p, const Smem& m, Sche
   }
   asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p.fetchLock), "r"(0u) : "memory");
   return false;
+}
+
+// Has every member of the collective's ring admitted submission `lo` of c?  One
+// slot per rank on the readiness board (reading R29), read with independent
+// relaxed loads -- a hint for the scheduler, not an ordering point.
+__device__ __noinline__ bool coll_ready(const DaemonParams& p, const RingDesc& R, int c, uint32_t lo) {
+  const int n = R.nranks;
+  if (n <= 1) return true;
+  const size_t off = (size_t)c * p.G * kFlagStride + kBoardOff;
+  for (int q0 = 0; q0 < n; q0 += 8) {
+    uint64_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = q0 + i < n ? ld_relaxed(R.flagsOf[q0 + i] + off, p.sysScope) : (uint64_t)lo;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if ((int32_t)((uint32_t)v[i] - lo) < 0) return false;
+  }
+  return true;
 }
 
 // One scheduling round: bookkeeping of the previous run, SQ fetch, entry
@@ -897,6 +930,29 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
     trace_at(p, *m.tr, b, kEvQuit, 0, 0);
     cmd = CMD_EXIT;
   } else if (qlen > 0) {
+    // Priority policy with the readiness board (reading R29): the highest-
+    // priority entry among the first kReadyScan that EVERY member rank admitted
+    // runs, with the full (boostable) threshold -- all ranks converge on it.  If
+    // none is ready, the traversal position of R10 is kept and the entry waits
+    // at most spinMin: a collective some rank has not even admitted cannot
+    // complete.
+    bool ready = true;
+    if (p.orderPolicy == 1 && p.readyFirst) {
+      const uint32_t scan = qlen < (uint32_t)kReadyScan ? qlen : (uint32_t)kReadyScan;
+      int pick = -1;
+      for (uint32_t i = 0; i < scan && pick < 0; ++i) {
+        const int ci = (int)(m.tq[i] & 0xffffu);
+        if (!m.ready[ci] && coll_ready(p, p.rings[m.subOf[ci]], ci, m.subLo[ci])) m.ready[ci] = 1;
+        if (m.ready[ci]) pick = (int)i;
+      }
+      if (pick >= 0) sh.pos = (uint32_t)pick;
+      else ready = false;
+    }
+    // only the front -- and with the board only a front every member admitted --
+    // is boosted and gets the full threshold; any other pick waits at most spinMin
+    // (a boosted non-front pick held its rank for up to spinCap while a higher-
+    // priority collective became ready elsewhere: live runs 2-3x slower)
+    sh.boostOk = p.orderPolicy == 1 ? (sh.pos == 0 && (!p.readyFirst || ready)) : 1;
     const int c = (int)(m.tq[sh.pos] & 0xffffu);
     const int way = c % W;
     sh.way = way;
@@ -922,8 +978,10 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
     // a lower-priority entry is visited only for as long as it progresses
     // (spinMin of waiting), so a rank does not hold a peer-less entry while the
     // others arrive at the front
-    if (p.stickiness && p.orderPolicy == 1 && sh.pos != 0) {
+    if (p.stickiness && p.orderPolicy == 1 && !sh.boostOk) {
       sh.T = p.spinMin;
+    } else if (p.stickiness && p.orderPolicy == 1) {
+      sh.T = p.spinBase;                              // the front / the first ready entry
     } else if (p.stickiness) {
       const uint64_t dec = (uint64_t)sh.pos * p.spinStep;
       uint64_t T = dec >= p.spinBase ? p.spinMin : p.spinBase - dec;
@@ -1086,7 +1144,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
       // a visit to a lower-priority entry keeps its short position threshold, so
       // progress a pair of neighbours makes on it (up to K slices) does not make
       // a rank stick to it for up to spinCap while the others wait at the front
-      if (p.stickiness && !(p.orderPolicy == 1 && sh.pos != 0)) {
+      if (p.stickiness && sh.boostOk) {
         T *= p.spinBoost;
         if (T > p.spinCap) T = p.spinCap;
       }
@@ -1831,6 +1889,9 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
   m.cacheTag = reinterpret_cast<int*>(m.cache + W);
   m.tq = reinterpret_cast<uint32_t*>(m.cacheTag + W);
   m.prio = reinterpret_cast<int32_t*>(m.tq + p.maxColl);
+  m.subLo = reinterpret_cast<uint32_t*>(m.prio + p.maxColl);
+  m.subOf = reinterpret_cast<uint8_t*>(m.subLo + p.maxColl);
+  m.ready = m.subOf + p.maxColl;
   m.tr = &pipe.tr;
   m.sqbuf = sqbuf;
   m.sqbar = &sqbar;
@@ -1852,6 +1913,7 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
     sh.lastSqPoll = 0;
     sh.sqPhase = 0;
     sh.needHostPoll = 0;
+    sh.boostOk = 1;
     mbar_init(&sqbar, 1);
     sh.lastRun = -1;
     sh.curId = -1;
@@ -1862,6 +1924,9 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
       m.tq[i] = p.tqSave[(size_t)b * p.maxColl + i];
       const int c = (int)(m.tq[i] & 0xffffu);
       m.prio[c] = p.ctx[(size_t)c * G + b].priority;
+      m.subLo[c] = (uint32_t)p.ctx[(size_t)c * G + b].s.subSeq;
+      m.subOf[c] = (uint8_t)p.ctx[(size_t)c * G + b].sub;
+      m.ready[c] = 0;
     }
     for (int w = 0; w < W; ++w) m.cacheTag[w] = -1;
     pipe.tr.base = p.traceCap ? p.traceCount[b] : 0;
@@ -1898,7 +1963,7 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
 
 extern "C" size_t occl_internal_daemon_smem(int maxColl, int cacheWays, int stages) {
   return (size_t)stages * sizeof(Stage) + (size_t)cacheWays * sizeof(CtxSlot) + (size_t)cacheWays * sizeof(int) +
-         (size_t)(maxColl + 1) * 4 + (size_t)maxColl * 4 + 16;
+         (size_t)(maxColl + 1) * 4 + (size_t)maxColl * 4 + (size_t)maxColl * (4 + 1 + 1) + 16;
 }
 
 // Two builds of the daemon: one block per SM (up to 640 threads) or two blocks

@@ -602,6 +602,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->l2Hints = 2;
   c->sqYieldNs = 20'000;
   c->llSpeculate = 0;
+  c->readyFirst = 1;
   return occlSuccess;
 }
 
@@ -766,6 +767,14 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
     c->peerIpc[prev] = c->prevIpc;
   }
   if (c->peerArena[c->rank] == nullptr) c->peerArena[c->rank] = c->arena;   // n == 1: own arena, not opened
+  // every other member's arena too: each rank reads all members' admissions on
+  // the readiness board (their flags, R29)
+  for (int q = 0; q < c->nranks; ++q) {
+    if (c->peerArena[q]) continue;
+    bool ipc = false;
+    if ((r = open(hs[q], &c->peerArena[q], &ipc)) != occlSuccess) return r;
+    c->peerIpc[q] = ipc ? 1 : 0;
+  }
   c->owner.assign(c->cfg.maxColl, nullptr);
   // ring 0: this communicator's own ring
   RingDesc rd{};
@@ -777,6 +786,8 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   rd.rank = c->rank;
   rd.directNext = c->cfg.directMode && !c->nextIpc && !c->cfg.forceSysScope;
   rd.directPrev = c->cfg.directMode && !c->prevIpc && !c->cfg.forceSysScope;
+  for (int q = 0; q < c->nranks; ++q)
+    rd.flagsOf[q] = (q == c->rank ? c->arena : c->peerArena[q]) + hs[q].flagsOffset;
   if (cudaMalloc(&c->ringsDev, kMaxRings * sizeof(RingDesc)) != cudaSuccess) return occlCudaError;
   if (cudaMemcpy(c->ringsDev, &rd, sizeof(rd), cudaMemcpyHostToDevice) != cudaSuccess) return occlCudaError;
   c->nrings = 1;
@@ -848,6 +859,7 @@ occlResult_t occlCommConnect(occlComm_t c, const void* all, size_t lenPerRank) {
   p.stallNs = c->cfg.stallNs;
   p.sqYieldNs = c->cfg.sqYieldNs;
   p.llSpeculate = c->cfg.llSpeculate;
+  p.readyFirst = c->cfg.readyFirst;
   Launcher* L = new Launcher();
   if ((r = launcher_start(L, {c})) != occlSuccess) {
     launcher_stop(L);
@@ -935,6 +947,12 @@ occlResult_t occlCommSplit(occlComm_t parent, int nmembers, const int* members, 
   rd.rank = me;
   rd.directNext = P->cfg.directMode && !P->peerIpc[nq] && !P->cfg.forceSysScope;
   rd.directPrev = P->cfg.directMode && !P->peerIpc[pq] && !P->cfg.forceSysScope;
+  for (int i = 0; i < nmembers; ++i) {                                // readiness board of every member
+    char* a = nullptr;
+    if (members[i] == P->rank) a = P->arena;
+    else if ((r = peer(members[i], &a)) != occlSuccess) return r;
+    rd.flagsOf[i] = a + P->handles[members[i]].flagsOffset;
+  }
   // the new entry is written before any submission names it (the SQE's release
   // store orders it for the daemon)
   // a destroyed child's slot is reused: the ids bound to it were retired

@@ -94,6 +94,7 @@ struct alignas(16) RingDesc {
   char* flagsPrev;     // upstream member's flags
   int32_t nranks, rank;
   int32_t directNext, directPrev;
+  char* flagsOf[kMaxRanks];   // every member's flags base, ring order (readiness board, R29)
 };
 
 // Static context: constant for one submission.  48 B.
@@ -231,6 +232,7 @@ struct DaemonParams {
   uint64_t stallNs;                 // FIFO: all entries stuck when none progressed for this long (0: off)
   uint64_t sqYieldNs;               // priority: host-SQ poll period of blocked collectives (0: no yield)
   int llSpeculate;                  // LL: issue recv slices before their lines arrived (abortable)
+  int readyFirst;                   // priority: run the highest-priority collective admitted by every member
   // CQ variant (NEXT-3 ablation): 0 = id slots (cqDone, default),
   // 1 = vanilla MPSC ring (entry, fence, in-order tail update), 2 = packed 64-bit
   // ring entries {stamp, id} (one host write, no fence between entry and tail)

@@ -56,7 +56,7 @@ class occlConfig_t(C.Structure):
         ("llSliceBytes", C.c_uint32), ("llMaxBytes", C.c_uint32), ("spinNs", C.c_uint32),
         ("bulkStores", C.c_int), ("directRead", C.c_int), ("stallNs", C.c_uint64),
         ("forceSysScope", C.c_int), ("cqMode", C.c_int), ("sqYieldNs", C.c_uint64),
-        ("llSpeculate", C.c_int),
+        ("llSpeculate", C.c_int), ("readyFirst", C.c_int),
     ]
 
 

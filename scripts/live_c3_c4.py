@@ -117,6 +117,9 @@ def main():
     ap.add_argument("--spin-min", type=int, default=0)
     ap.add_argument("--spin-cap", type=int, default=0)
     ap.add_argument("--quit-idle-ns", type=int, default=0)
+    ap.add_argument("--ready-first", type=int, default=-1, help="-1: library default")
+    ap.add_argument("--c3-gap", choices=["op", "zero"], default="op",
+                    help="C3 inter-submission gap: Exp(one op) or back-to-back (SURVEY §8(d) C3)")
     ap.add_argument("--tag", default="")
     args = ap.parse_args()
     torch.cuda.set_device(0)
@@ -136,6 +139,8 @@ def main():
                     extra[k] = v
             if args.spin_step >= 0:
                 extra["spinStep"] = args.spin_step
+            if args.ready_first >= 0:
+                extra["readyFirst"] = args.ready_first
             comms = harness.ring(n, 0, gridBlocks=args.grid, maxColl=256, orderPolicy=policy, stickiness=stick,
                                  **extra)
             fifo = policy == 0
@@ -153,6 +158,8 @@ def main():
                 t_cal, _, _ = one(comms, jobs, n, ncoll, 1, seed, 99, 0.0, "consistent")
                 t_cal, _, _ = one(comms, jobs, n, ncoll, 1, seed, 98, 0.0, "consistent")
                 mean_gap = t_cal / 1e3 / ncoll
+                if wname == "c3" and args.c3_gap == "zero":
+                    mean_gap = 0.0
                 for rep in range(args.repeats):
                     tc, sc, rc = one(comms, jobs, n, ncoll, iters, seed, rep, mean_gap, "consistent")
                     tr, sr, rr = one(comms, jobs, n, ncoll, iters, seed, rep, mean_gap, "random")
