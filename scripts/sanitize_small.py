@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Small end-to-end run of the daemon for compute-sanitizer (memcheck /
-synccheck / racecheck): every kind, Simple and LL, direct mode on and off, a
-sub-communicator, checked bit-exactly against the oracle.  Sizes are tiny so
+synccheck / racecheck): every kind, Simple and LL (with and without LL
+speculation), direct mode on and off, a sub-communicator, the TMA SQ fetch and
+the readiness board, checked bit-exactly against the oracle.  Sizes are tiny so
 the instrumented persistent kernel finishes in minutes.
 
   compute-sanitizer --tool memcheck python scripts/sanitize_small.py
@@ -24,9 +25,12 @@ def main():
     U.WAIT_S = 600.0
     n = 4
     runs = 0
-    for direct, llmax in [(1, 64 << 10), (0, 0)]:
+    # (direct mode, LL limit, LL speculation): Simple + LL with direct mode, Simple-only
+    # connector path, LL with speculation (abortable data-warp polling); the default
+    # priority policy with the readiness board throughout
+    for direct, llmax, spec in [(1, 64 << 10, 0), (0, 0, 0), (1, 64 << 10, 1)]:
         comms = occl.local_group(n, 0, gridBlocks=2, maxColl=8, sliceBytes=16 << 10, stagingTiles=2,
-                                 directMode=direct, llMaxBytes=llmax, quitIdleNs=500_000)
+                                 directMode=direct, llMaxBytes=llmax, llSpeculate=spec, quitIdleNs=500_000)
         try:
             for ci, (kind, dtype, count) in enumerate([("allreduce", "f32", 20_003), ("allreduce", "bf16", 3_001),
                                                        ("allgather", "i32", 5_001), ("reducescatter", "f32", 4_099),
