@@ -82,3 +82,27 @@ def test_product_path_never_touches_oracle():
             if f.endswith((".py", ".cu", ".cc", ".h")):
                 s = open(os.path.join(dp, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle\b|oracle/|oracle\.", s, re.M), f
+
+
+def test_daemon_register_budget():
+    """The data warps must not spill (their loop is the bandwidth path) and the
+    control thread's spills stay bounded: a call placed in the control thread's
+    hot loop once made it spill its live state and cost 27 % of the bench's busbw
+    (round-2 changes).  ptxas -v on the daemon, same flags as build.py."""
+    import re
+    from paper_2303_06324_b200 import build as b
+    src = os.path.join(b.CSRC, "occl_daemon.cu")
+    r = subprocess.run([b.NVCC] + b.ARCH + ["-O3", "-std=c++17", "-I" + os.path.join(b.ROOT, "include"),
+                                            "-Xptxas", "-v", "-maxrregcount=104", "-c", src, "-o", os.devnull],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
+    spills = {}
+    lines = r.stderr.splitlines()
+    for i, l in enumerate(lines):
+        m = re.search(r"Function properties for \S*?(compute_main|control_main|publisher_main|producer_main)", l)
+        if m and i + 1 < len(lines) and m.group(1) not in spills:      # first build: 1 block per SM
+            s = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", lines[i + 1])
+            spills[m.group(1)] = (int(s.group(1)), int(s.group(2)))
+    assert spills["compute_main"] == (0, 0) and spills["publisher_main"] == (0, 0), spills
+    assert spills["producer_main"] == (0, 0), spills
+    assert spills["control_main"][0] <= 320 and spills["control_main"][1] <= 320, spills
