@@ -30,7 +30,10 @@ It follows the paper's algorithm step by step (§3 "Design", §4
   #CQE < #SQE;
 * stickiness: FIFO or priority-front ordering; initial spin
   threshold decremented by queue position, raised on each successful primitive
-  (PAPER.md:449-452);
+  (PAPER.md:449-452); optionally the readiness-board extension of the priority
+  policy (ready_first, reading R29 -- not in the paper, labelled): at
+  switch-in the first entry every member of its ring admitted runs, and only a
+  ready front is boosted;
 * "baseline" mode is the NCCL-like negative control: infinite
   threshold, no quit, a fixed number of resident slots ("streams", Fig. 1(b)),
   strictly in submission order.
@@ -63,6 +66,8 @@ class SimConfig:
     slices_per_chunk: int = 4
     order_policy: str = "fifo"     # "fifo" | "priority"
     priority_cadence: int = 4      # priority policy: check SQ every R lane ticks
+    ready_first: bool = False      # priority policy extension (reading R29): at switch-in run
+                                   # the highest-priority entry (among the first 8) every member admitted
     stickiness: bool = True        # paper's spin-threshold policy; False = constant T
     spin_base: int = 4096          # SPEC.md:421 desk-scale defaults
     spin_step: int = 256
@@ -165,6 +170,7 @@ class _Lane:
     queue: list = field(default_factory=list)
     pos: int = 0
     T: float | None = None         # live spin threshold of the current visit
+    boost_ok: bool = True          # ready_first: the current visit may be boosted
     spins: int = 0
     stall: dict = field(default_factory=dict)
     clock: int = 0
@@ -185,6 +191,7 @@ class _Rank:
     static: dict = field(default_factory=dict)    # (coll, lane) -> _Static
     dyn_global: dict = field(default_factory=dict)  # (coll, lane) -> _Dyn (context buffer)
     outstanding: dict = field(default_factory=dict)  # coll -> submission count in flight
+    adm: dict = field(default_factory=dict)       # (coll, lane) -> admissions so far (readiness board, R29)
     program: list = field(default_factory=list)
     pc: int = 0
     delay_until: int = 0
@@ -293,6 +300,7 @@ class Simulator:
         self.last_progress = 0
         # statistics (reported, not asserted: parity unpinned)
         self.preempt = {}              # (rank, coll, lane) -> count
+        self.ready_picks_behind_front = 0   # R29 switch-ins that ran a ready entry behind the queue front
         self.loads = 0
         self.saves = 0
         self.launches = [0] * nranks
@@ -416,6 +424,7 @@ class Simulator:
         R.static[(m.coll_id, b)] = _Static(m, rr, n, seq, segs, part, b, nloops,
                                            sqe.sendbuf, sqe.recvbuf, sqe.sub_index, members)
         R.dyn_global[(m.coll_id, b)] = _Dyn()
+        R.adm[(m.coll_id, b)] = R.adm.get((m.coll_id, b), 0) + 1
         way = m.coll_id % self.cfg.cache_ways
         if way in L.cache and L.cache[way][0] == m.coll_id:
             del L.cache[way]
@@ -530,6 +539,24 @@ class Simulator:
             return True
         # (2) execute the entry at the current position
         if L.queue:
+            ready_first = c.ready_first and c.order_policy == "priority" and not c.baseline
+            if L.T is None and ready_first:
+                # switch-in under the readiness board (R29): the first entry every
+                # member of its ring admitted wins and, if it is the front, runs with
+                # the full boostable threshold; otherwise the entry at pos waits
+                # at most spin_min
+                pick = None
+                for i, cid in enumerate(L.queue[:8]):
+                    need = R.adm[(cid, b)]
+                    if all(self.ranks[q].adm.get((cid, b), 0) >= need for q in R.static[(cid, b)].members):
+                        pick = i
+                        break
+                if pick is not None:
+                    L.pos = pick
+                    if pick > 0:
+                        self.ready_picks_behind_front += 1
+                L.boost_ok = pick == 0
+                L.T = c.spin_base if L.boost_ok else c.spin_min
             coll = L.queue[L.pos]
             st = R.static[(coll, b)]
             d = self._load_ctx(r, b, coll)
@@ -538,7 +565,8 @@ class Simulator:
             if self._try_slice(r, b, st, d):
                 L.spins = 0
                 L.stall[coll] = 0
-                L.T = boosted_threshold(L.T, c)
+                if not ready_first or L.boost_ok:
+                    L.T = boosted_threshold(L.T, c)
                 if self._advance(st, d):
                     self._complete(r, b, coll)
                 return True

@@ -182,6 +182,44 @@ def test_bruteforce_all_orders_complete(n, k):
 
 
 @pytest.mark.parametrize("n,k", [(2, 2), (2, 3), (3, 2), (3, 3)])
+def test_bruteforce_all_orders_ready_first(n, k):
+    """The readiness-board rule (R29: run the highest-priority entry every
+    member admitted; a non-ready or non-front pick waits spin_min and is not
+    boosted) keeps deadlock freedom: every (k!)^n order set completes, outputs
+    bit-exact, exactly once, with the rule actually steering (some switch-in picks
+    an entry behind the queue front)."""
+    metas = _small_metas(k)
+    sets = _all_order_sets(n, k)
+    steered = 0
+    for si, orders in enumerate(sets):
+        T = (1, 3, 64)[si % 3]
+        cfg = dfce.SimConfig(spin_base=T, spin_step=max(1, T // 8), spin_min=1, spin_cap=4 * T,
+                             stickiness=bool((si // 3) % 2), order_policy="priority", ready_first=True,
+                             seed=si, **_BF_CFG)
+        sim, bufs = dfce.run_orders(metas, [list(o) for o in orders], cfg, seed=si)
+        _check_results(sim, bufs, metas, n)
+        _check_accounting(sim, metas, n)
+        steered += sim.ready_picks_behind_front
+    assert steered > 0
+
+
+def test_subcommunicators_all_orders_ready_first():
+    """R29 on overlapping sub-communicator rings: readiness is per ring (its own
+    members' admissions); all 216 per-rank order sets complete exactly."""
+    n, metas = 3, _sub_metas()
+    sets = _sub_order_sets(metas, n)
+    for si, orders in enumerate(sets):
+        T = (1, 3, 64)[si % 3]
+        cfg = dfce.SimConfig(spin_base=T, spin_step=max(1, T // 8), spin_min=1, spin_cap=4 * T,
+                             stickiness=bool(si % 2), order_policy="priority", ready_first=True,
+                             seed=si, **_BF_CFG)
+        sim, bufs = dfce.run_orders(metas, orders, cfg, seed=si)
+        _check_sub_results(sim, bufs, metas, n)
+        for r in range(n):
+            assert len(sim.ranks[r].cq) == sim.ranks[r].submitted
+
+
+@pytest.mark.parametrize("n,k", [(2, 2), (2, 3), (3, 2), (3, 3)])
 def test_bruteforce_every_variant_small(n, k):
     """Each (threshold, stickiness, policy) variant on a deterministic sample of sets."""
     metas = _small_metas(k)
