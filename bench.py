@@ -65,7 +65,6 @@ def parse():
     ap.add_argument("--slices-per-chunk", type=int, default=2)
     ap.add_argument("--threads", type=int, default=608)
     ap.add_argument("--pipe-depth", type=int, default=4)
-    ap.add_argument("--prefetch", type=int, default=0)
     ap.add_argument("--discard", type=int, default=1)
     ap.add_argument("--l2-hints", type=int, default=2)
     ap.add_argument("--direct", type=int, default=1)
@@ -240,7 +239,7 @@ def bench_cfg(args, **extra):
     from paper_2303_06324_b200 import occl
     kw = dict(gridBlocks=args.grid_blocks, sliceBytes=args.slice_kib * 1024, connSlots=args.conn_slots,
               slicesPerChunk=args.slices_per_chunk, blockThreads=args.threads, pipeDepth=args.pipe_depth,
-              prefetchSlices=args.prefetch, discardConsumed=args.discard, l2Hints=args.l2_hints,
+              discardConsumed=args.discard, l2Hints=args.l2_hints,
               directMode=args.direct, stagingTiles=args.stages, blocksPerSM=args.blocks_per_sm,
               bulkStores=args.bulk_stores, directRead=args.direct_read, maxColl=128, autoLaunch=0,
               orderPolicy=args.order_policy, forceSysScope=args.force_sys)
@@ -474,7 +473,7 @@ def run_single(args, world, prank, local, dist):
                    "ranks": R, "ranks_per_gpu": V, "size_bytes_per_rank": size, "grid_blocks": args.grid_blocks,
                    "slice_bytes": args.slice_kib * 1024, "conn_slots": args.conn_slots,
                    "slices_per_chunk": args.slices_per_chunk, "block_threads": args.threads,
-                   "pipe_depth": args.pipe_depth, "staging_tiles": args.stages, "prefetch_slices": args.prefetch, "l2": "inputs larger than L2 (R x S >> 126 MB)",
+                   "pipe_depth": args.pipe_depth, "staging_tiles": args.stages, "l2": "inputs larger than L2 (R x S >> 126 MB)",
                    "algbw_GBps": size / (ms_step / 1e3) / 1e9},
         "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -104,7 +104,8 @@ typedef struct {
   int autoLaunch;         /* 1 = event-driven (re)start by the host supervisor */
   int cacheWays;          /* direct-mapped shared-memory context cache ways        */
   int pipeDepth;          /* slices in flight between the control warp and the data warps (1..8)   */
-  int prefetchSlices;     /* send-buffer slices prefetched into L2 ahead of the issue cursor      */
+  int prefetchSlices;     /* reserved, must be 0 (an L2 prefetch of the send-buffer operand measured
+                             8-14 % slower and was removed)                          */
   int discardConsumed;    /* 1 = drop consumed connector lines from L2 without write-back         */
   int l2Hints;            /* 1 = evict-first L2 policy for send/recv-buffer streams; 2 = also evict-last for connector stores;
                              3 = also evict-last for direct sends the downstream forwards (demoted once read) */

@@ -1087,8 +1087,6 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   // ---- dynamic context -> registers
   Cursor dc{cx.d.loop, cx.d.step, cx.d.slc, cx.d.nsent, cx.d.nrecv};
   Cursor di = dc;
-  Cursor dpf = dc;                                        // L2 prefetch cursor (runs ahead of di)
-  uint32_t pfAhead = 0;
   const uint64_t laneLo = (uint64_t)cx.lane * part;
   uint64_t headSeen = 0, creditSeen = 0;
   // spins are counted in time: T x spinNs of failed polling (R1) --
@@ -1294,36 +1292,6 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     ++issued;
     prepared = false;
     advance(di, prim, spc, nsteps);
-    if (pfAhead) --pfAhead;
-    // ---- prefetch the send-buffer operand of the slices ahead into L2 (TMA
-    // prefetch): it has no peer dependency, so the loads on the critical path
-    // of the ring hop hit L2 instead of DRAM
-    while (pfAhead < (uint32_t)p.prefetchSlices && dpf.loop < nloops) {
-      if (dpf.loop < di.loop || (dpf.loop == di.loop && (dpf.step < di.step ||
-                                                         (dpf.step == di.step && dpf.slc < di.slc)))) {
-        dpf = di;                                         // never prefetch behind the issue cursor
-      }
-      int pprim, pseg;
-      step_prim(kind, n, r, root, dpf.step, inplace, pprim, pseg);
-      pprim = directify(pprim, kind, n, dpf.step, dOut, dIn, dRead);
-      if ((pprim & A_REDUCE) || !(pprim & A_RECV)) {      // primitive reads the send buffer
-        uint64_t so, ro, ln;
-        seg_geom(kind, n, r, count, segLen, pseg, so, ro, ln);
-        uint64_t lh = laneLo + part;
-        if (lh > ln) lh = ln;
-        const uint64_t plo = laneLo + ((uint64_t)dpf.loop * spc + dpf.slc) * E;
-        uint64_t phi = plo + E;
-        if (phi > lh) phi = lh;
-        if (phi > plo) {
-          const char* a = reinterpret_cast<const char*>(sendbuff) + (so + plo) * isz;
-          const uint64_t bytes = ((phi - plo) * isz) & ~(uint64_t)15;
-          if (bytes && !((uintptr_t)a & 15))
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a), "r"((uint32_t)bytes) : "memory");
-        }
-      }
-      advance(dpf, pprim, spc, nsteps);
-      ++pfAhead;
-    }
   }
   // ---- registers -> dynamic context in the shared-memory cache
   if (nSlices) cx.d.progressed = 1;

@@ -388,7 +388,7 @@ occlResult_t validate_config(const occlConfig_t& c) {
   if (c.priorityCadence < 1) return occlInvalidArgument;
   if (c.stallLimit < 1) return occlInvalidArgument;
   if (c.pipeDepth < 1 || c.pipeDepth > 8) return occlInvalidArgument;
-  if (c.prefetchSlices < 0 || c.prefetchSlices > 64) return occlInvalidArgument;
+  if (c.prefetchSlices != 0) return occlInvalidArgument;       // reserved (the L2 prefetch was removed)
   if (c.stagingTiles < 1 || c.stagingTiles > 6) return occlInvalidArgument;
   if (c.l2Hints < 0 || c.l2Hints > 3) return occlInvalidArgument;
   if (c.cqMode < 0 || c.cqMode > 2) return occlInvalidArgument;

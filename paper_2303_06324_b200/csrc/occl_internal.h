@@ -211,7 +211,7 @@ struct DaemonParams {
   int cacheWays;
   int sysScope;                     // 1: peers in other processes/devices -> .sys fences
   int pipeDepth;                    // slices in flight control -> data warps (<= 8)
-  int prefetchSlices;               // L2 prefetch distance for the send-buffer operand (slices)
+  int prefetchSlices;               // reserved (0): the L2 prefetch of the send-buffer operand was removed
   int discardConsumed;              // invalidate consumed connector lines in L2 (no write-back)
   int directNext;                   // downstream's buffers are addressable: final data goes straight there
   int directPrev;                   // upstream writes final data straight into our recv buffer
