@@ -412,13 +412,18 @@ int coll_blocks(const occlComm* c, int kind, size_t count, int dtype) {
   uint64_t nb = (bytes + c->cfg.minBlockBytes - 1) / c->cfg.minBlockBytes;
   if (nb < 1) nb = 1;
   if (nb > G) nb = G;
-  // Latency-bound collectives (the whole segment fits in one LL slice per block
-  // of the grid): spread them so every block moves ONE LL slice per step.  A
-  // ring step then costs one LL hop (~3 us at 8 ranks) whatever the size, where
+  // Latency-bound collectives -- those the block rule above already sends over
+  // LL (per-block part <= llMaxBytes) -- are spread so every block moves ONE LL
+  // slice per step: a ring step then costs one LL hop (~3 us at 8 ranks), where
   // a single block would chain several slices per step (a 256 KiB all-reduce at
   // 8 ranks: 4 slices x 14 steps on one block, slower than 1 MiB on Simple).
+  // Collectives the block rule sends over Simple keep their block count: LL on
+  // the whole grid would cut a 1 MiB all-reduce's single-op latency but also
+  // its pipelined throughput (4.6x, several ops can no longer share the grid).
   // Same on every rank: a function of (count, dtype, nranks, config).
-  if (c->cfg.llMaxBytes && c->nranks > 1 && bytes <= G * (uint64_t)c->cfg.llSliceBytes) {
+  const uint64_t partBytes = (bytes + nb - 1) / nb;
+  if (c->cfg.llMaxBytes && c->nranks > 1 && partBytes <= c->cfg.llMaxBytes &&
+      bytes <= G * (uint64_t)c->cfg.llSliceBytes) {
     uint64_t nbLL = (bytes + c->cfg.llSliceBytes - 1) / c->cfg.llSliceBytes;
     if (nbLL > nb) nb = nbLL;
   }
