@@ -133,10 +133,12 @@ typedef struct {
                              whose lines do not come within the spin threshold is aborted and redone
                              later (LL lines are idempotent to rewrite).  0 = the control lane polls the
                              slice's last line first */
-  int readyFirst;         /* priority policy: run the highest-priority collective that EVERY member
+  int readyFirst;         /* priority policy: 1/2 = run the highest-priority collective that EVERY member
                              rank has admitted (each rank publishes its admissions on a readiness
                              board in its flags; R29); a collective not yet admitted
-                             everywhere waits at most spinMin.  0 = the queue front first (R10) */
+                             everywhere waits at most spinMin (1), or -- when the whole queue is in
+                             the scan window and nothing in it is ready -- is not run at all while
+                             the block waits for admissions (2).  0 = the queue front first (R10) */
 } occlConfig_t;
 
 /* Aggregate counters (device counters summed over blocks/collectives). */

@@ -888,7 +888,24 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
     }
     if (fetched) return CMD_NONE;
   }
-  const bool stuck = qlen == 0 || allStalled;
+  // Readiness scan (reading R29, priority policy): the highest-priority entry
+  // among the first kReadyScan that EVERY member rank admitted.  With
+  // readyFirst = 2 and the whole queue inside the scan window, a queue with no
+  // ready entry is not run at all -- none of its collectives can complete -- and
+  // the block waits like an idle one (and counts as stuck for the quit vote);
+  // with readyFirst = 1 its entries are visited for spinMin each.
+  int readyPick = -1;
+  bool waitReady = false;
+  if (qlen > 0 && p.orderPolicy == 1 && p.readyFirst) {
+    const uint32_t scan = qlen < (uint32_t)kReadyScan ? qlen : (uint32_t)kReadyScan;
+    for (uint32_t i = 0; i < scan && readyPick < 0; ++i) {
+      const int ci = (int)(m.tq[i] & 0xffffu);
+      if (!m.ready[ci] && coll_ready(p, p.rings[m.subOf[ci]], ci, m.subLo[ci])) m.ready[ci] = 1;
+      if (m.ready[ci]) readyPick = (int)i;
+    }
+    waitReady = readyPick < 0 && p.readyFirst >= 2 && qlen <= (uint32_t)kReadyScan;
+  }
+  const bool stuck = qlen == 0 || allStalled || waitReady;
   // Voluntary quit is decided for the whole launch: a block
   // that has been stuck or idle for quitIdleNs only VOTES; the launch quits once
   // every block voted (a block gone alone would strand the SQEs of its lanes --
@@ -929,23 +946,15 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
     p.blkStats[b].quits++;                           // voluntary quit
     trace_at(p, *m.tr, b, kEvQuit, 0, 0);
     cmd = CMD_EXIT;
-  } else if (qlen > 0) {
-    // Priority policy with the readiness board (reading R29): the highest-
-    // priority entry among the first kReadyScan that EVERY member rank admitted
-    // runs, with the full (boostable) threshold -- all ranks converge on it.  If
-    // none is ready, the traversal position of R10 is kept and the entry waits
-    // at most spinMin: a collective some rank has not even admitted cannot
+  } else if (qlen > 0 && !waitReady) {
+    // Priority policy with the readiness board (reading R29): the ready entry of
+    // the scan runs, with the full (boostable) threshold -- all ranks converge on
+    // it.  If none is ready, the traversal position of R10 is kept and the entry
+    // waits at most spinMin: a collective some rank has not even admitted cannot
     // complete.
     bool ready = true;
     if (p.orderPolicy == 1 && p.readyFirst) {
-      const uint32_t scan = qlen < (uint32_t)kReadyScan ? qlen : (uint32_t)kReadyScan;
-      int pick = -1;
-      for (uint32_t i = 0; i < scan && pick < 0; ++i) {
-        const int ci = (int)(m.tq[i] & 0xffffu);
-        if (!m.ready[ci] && coll_ready(p, p.rings[m.subOf[ci]], ci, m.subLo[ci])) m.ready[ci] = 1;
-        if (m.ready[ci]) pick = (int)i;
-      }
-      if (pick >= 0) sh.pos = (uint32_t)pick;
+      if (readyPick >= 0) sh.pos = (uint32_t)readyPick;
       else ready = false;
     }
     // only the front -- and with the board only a front every member admitted --
