@@ -66,8 +66,10 @@ class SimConfig:
     slices_per_chunk: int = 4
     order_policy: str = "fifo"     # "fifo" | "priority"
     priority_cadence: int = 4      # priority policy: check SQ every R lane ticks
-    ready_first: bool = False      # priority policy extension (reading R29): at switch-in run
-                                   # the highest-priority entry (among the first 8) every member admitted
+    ready_first: int = 0           # priority policy extension (reading R29): at switch-in run
+                                   # the highest-priority entry (among the first 8) every member admitted;
+                                   # 2 = a lane whose whole queue is scanned and has no ready entry runs
+                                   # nothing (waits; counts as stuck for the quit rule)
     stickiness: bool = True        # paper's spin-threshold policy; False = constant T
     spin_base: int = 4096          # SPEC.md:421 desk-scale defaults
     spin_step: int = 256
@@ -171,6 +173,7 @@ class _Lane:
     pos: int = 0
     T: float | None = None         # live spin threshold of the current visit
     boost_ok: bool = True          # ready_first: the current visit may be boosted
+    waiting: bool = False          # ready_first = 2: nothing in the queue is ready
     spins: int = 0
     stall: dict = field(default_factory=dict)
     clock: int = 0
@@ -301,6 +304,7 @@ class Simulator:
         # statistics (reported, not asserted: parity unpinned)
         self.preempt = {}              # (rank, coll, lane) -> count
         self.ready_picks_behind_front = 0   # R29 switch-ins that ran a ready entry behind the queue front
+        self.ready_waits = 0                # R29 wait mode: lane ticks with nothing ready to run
         self.loads = 0
         self.saves = 0
         self.launches = [0] * nranks
@@ -551,6 +555,11 @@ class Simulator:
                     if all(self.ranks[q].adm.get((cid, b), 0) >= need for q in R.static[(cid, b)].members):
                         pick = i
                         break
+                L.waiting = pick is None and c.ready_first >= 2 and len(L.queue) <= 8
+                if L.waiting:                     # none can complete: run nothing (R29, wait mode)
+                    self.ready_waits += 1
+                    self._quit_check(r, b)
+                    return False
                 if pick is not None:
                     L.pos = pick
                     if pick > 0:
@@ -598,7 +607,7 @@ class Simulator:
         R, L, c = self.ranks[r], self.ranks[r].lanes[b], self.cfg
         if not c.quit_enabled or c.baseline:
             return
-        stuck = (not L.queue) or all(L.stall.get(i, 0) >= c.stall_limit for i in L.queue)
+        stuck = (not L.queue) or all(L.stall.get(i, 0) >= c.stall_limit for i in L.queue) or L.waiting
         if stuck and L.clock - L.last_fetch >= c.quit_idle:
             for coll in L.queue:              # contexts already saved at preemption
                 way = coll % c.cache_ways

@@ -181,8 +181,9 @@ def test_bruteforce_all_orders_complete(n, k):
         _check_accounting(sim, metas, n)
 
 
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("n,k", [(2, 2), (2, 3), (3, 2), (3, 3)])
-def test_bruteforce_all_orders_ready_first(n, k):
+def test_bruteforce_all_orders_ready_first(n, k, mode):
     """The readiness-board rule (R29: run the highest-priority entry every
     member admitted; a non-ready or non-front pick waits spin_min and is not
     boosted) keeps deadlock freedom: every (k!)^n order set completes, outputs
@@ -190,20 +191,23 @@ def test_bruteforce_all_orders_ready_first(n, k):
     an entry behind the queue front)."""
     metas = _small_metas(k)
     sets = _all_order_sets(n, k)
-    steered = 0
+    steered = waited = 0
     for si, orders in enumerate(sets):
         T = (1, 3, 64)[si % 3]
         cfg = dfce.SimConfig(spin_base=T, spin_step=max(1, T // 8), spin_min=1, spin_cap=4 * T,
-                             stickiness=bool((si // 3) % 2), order_policy="priority", ready_first=True,
+                             stickiness=bool((si // 3) % 2), order_policy="priority", ready_first=mode,
                              seed=si, **_BF_CFG)
         sim, bufs = dfce.run_orders(metas, [list(o) for o in orders], cfg, seed=si)
         _check_results(sim, bufs, metas, n)
         _check_accounting(sim, metas, n)
         steered += sim.ready_picks_behind_front
+        waited += sim.ready_waits
     assert steered > 0
+    assert (waited > 0) == (mode == 2)
 
 
-def test_subcommunicators_all_orders_ready_first():
+@pytest.mark.parametrize("mode", [1, 2])
+def test_subcommunicators_all_orders_ready_first(mode):
     """R29 on overlapping sub-communicator rings: readiness is per ring (its own
     members' admissions); all 216 per-rank order sets complete exactly."""
     n, metas = 3, _sub_metas()
@@ -211,7 +215,7 @@ def test_subcommunicators_all_orders_ready_first():
     for si, orders in enumerate(sets):
         T = (1, 3, 64)[si % 3]
         cfg = dfce.SimConfig(spin_base=T, spin_step=max(1, T // 8), spin_min=1, spin_cap=4 * T,
-                             stickiness=bool(si % 2), order_policy="priority", ready_first=True,
+                             stickiness=bool(si % 2), order_policy="priority", ready_first=mode,
                              seed=si, **_BF_CFG)
         sim, bufs = dfce.run_orders(metas, orders, cfg, seed=si)
         _check_sub_results(sim, bufs, metas, n)
