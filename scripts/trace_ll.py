@@ -68,13 +68,23 @@ def main():
                 if sw and dn:
                     exe.append((dn[-1] - sw[0]) / 1e3)
                     adm.append((sw[0] - evs[r][0][0]) / 1e3)
+        # one sample's timeline on the lane-0 block of rank 0 and of rank 7: every
+        # event from 30 us before the fetch of the last submission to its switch-in
+        timeline = {}
+        for rk in (0, n - 1):
+            tr = comms[rk].trace(cid % a.grid)
+            f = max(i for i, (t, e, c, x) in enumerate(tr) if e == "fetch" and c == cid)
+            t0 = tr[f][0]
+            sw = next((i for i in range(f, len(tr)) if tr[i][1] == "switch_in"), len(tr) - 1)
+            timeline[rk] = [(round((t - t0) / 1e3, 2), e, c, x) for t, e, c, x in tr
+                            if t0 - 30_000 <= t <= tr[sw][0]]
         res = {"bytes": a.bytes, "hops_sampled": len(det),
                "detect_us_median": statistics.median(det) if det else None,
                "detect_us_p10": sorted(det)[len(det) // 10] if det else None,
                "move_us_median": statistics.median(mov) if mov else None,
                "execute_us_median": statistics.median(exe) if exe else None,
                "fetch_to_switchin_us_median": statistics.median(adm) if adm else None,
-               "issues_per_rank": len(issue[0])}
+               "issues_per_rank": len(issue[0]), "timeline_lane0_block": timeline}
         print(json.dumps(res))
         with open(a.out, "w") as f:
             json.dump(res, f)
