@@ -78,7 +78,20 @@ def main():
             sw = next((i for i in range(f, len(tr)) if tr[i][1] == "switch_in"), len(tr) - 1)
             timeline[rk] = [(round((t - t0) / 1e3, 2), e, c, x) for t, e, c, x in tr
                             if t0 - 30_000 <= t <= tr[sw][0]]
-        res = {"bytes": a.bytes, "hops_sampled": len(det),
+        # the same sample on every rank: fetch (admission), switch-in, done, CQE, relative
+        # to the earliest admission (all ranks share %globaltimer)
+        per_rank = {}
+        for rk in range(n):
+            tr = comms[rk].trace(cid % a.grid)
+            f = max(i for i, (t, e, c, x) in enumerate(tr) if e == "fetch" and c == cid)
+            ev = {}
+            for t, e, c, x in tr[f:]:
+                if e in ("fetch", "switch_in", "done", "cqe") and e not in ev:
+                    ev[e] = t
+            per_rank[rk] = ev
+        tmin = min(v["fetch"] for v in per_rank.values())
+        per_rank = {rk: {e: round((t - tmin) / 1e3, 2) for e, t in v.items()} for rk, v in per_rank.items()}
+        res = {"bytes": a.bytes, "hops_sampled": len(det), "per_rank_last_sample_us": per_rank,
                "detect_us_median": statistics.median(det) if det else None,
                "detect_us_p10": sorted(det)[len(det) // 10] if det else None,
                "move_us_median": statistics.median(mov) if mov else None,
