@@ -476,7 +476,7 @@ constexpr uint32_t kQuitLatch = 0x80000000u;   // quitWord: every block of the l
 constexpr uint64_t kSqPollNs = 2000;           // a blocked collective polls the SQ at most this often
 constexpr int kSqBurst = 4;                    // host SQ slots read by one bulk copy
 constexpr int kBoardOff = kDirectOff + 64;     // readiness board slot in the (collId, block 0) direct line
-constexpr int kReadyScan = 8;                  // queue entries the priority scheduler checks for readiness
+constexpr int kReadyScan = 64;                 // queue entries the priority scheduler checks for readiness
 
 // Scheduler state of one block; touched only by the control thread.
 struct Sched {
@@ -744,6 +744,50 @@ __device__ __noinline__ bool coll_ready(const DaemonParams& p, const RingDesc& R
   return true;
 }
 
+// The first of the first `lim` queue entries (priority order) that every member
+// admitted, or -1.  Entries are checked two at a time: the board loads of
+// a pair (up to 2 x 8 ranks) are issued together, so a scan costs one round trip
+// per pair, not per entry; an entry once seen ready stays ready for its
+// submission (m.ready).
+__device__ __noinline__ int ready_scan(const DaemonParams& p, const Smem& m, uint32_t lim) {
+  for (uint32_t i0 = 0; i0 < lim; i0 += 2) {
+    int rdy[2];
+    uint64_t v[2][8];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      rdy[j] = 0;
+      const uint32_t i = i0 + j;
+      if (i >= lim) continue;
+      const int ci = (int)(m.tq[i] & 0xffffu);
+      if (m.ready[ci]) { rdy[j] = 1; continue; }
+      const RingDesc& R = p.rings[m.subOf[ci]];
+      const int n = R.nranks;
+      rdy[j] = n <= 8 ? 2 : 3;                       // 2: decide from v[j]; 3: more than 8 members
+      const size_t off = (size_t)ci * p.G * kFlagStride + kBoardOff;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[j][q] = q < n ? ld_relaxed(R.flagsOf[q] + off, p.sysScope) : ~0ull;
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint32_t i = i0 + j;
+      if (i >= lim) break;
+      const int ci = (int)(m.tq[i] & 0xffffu);
+      if (rdy[j] == 2) {
+        bool ok = true;
+        const uint32_t lo = m.subLo[ci];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) ok = ok && (v[j][q] == ~0ull || (int32_t)((uint32_t)v[j][q] - lo) >= 0);
+        if (ok) { m.ready[ci] = 1; rdy[j] = 1; }
+      } else if (rdy[j] == 3 && coll_ready(p, p.rings[m.subOf[ci]], ci, m.subLo[ci])) {
+        m.ready[ci] = 1;
+        rdy[j] = 1;
+      }
+      if (rdy[j] == 1) return (int)i;
+    }
+  }
+  return -1;
+}
+
 // One scheduling round: bookkeeping of the previous run, SQ fetch, entry
 // selection, voluntary quit.  Returns CMD_*.
 __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, const Smem& m) {
@@ -897,13 +941,12 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
   int readyPick = -1;
   bool waitReady = false;
   if (qlen > 0 && p.orderPolicy == 1 && p.readyFirst) {
-    const uint32_t scan = qlen < (uint32_t)kReadyScan ? qlen : (uint32_t)kReadyScan;
-    for (uint32_t i = 0; i < scan && readyPick < 0; ++i) {
-      const int ci = (int)(m.tq[i] & 0xffffu);
-      if (!m.ready[ci] && coll_ready(p, p.rings[m.subOf[ci]], ci, m.subLo[ci])) m.ready[ci] = 1;
-      if (m.ready[ci]) readyPick = (int)i;
-    }
-    waitReady = readyPick < 0 && p.readyFirst >= 2 && qlen <= (uint32_t)kReadyScan;
+    // (a round trip per pair of not-yet-ready entries; tried alternatives -- 8
+    // entries, 8 every round + 64 every 4th -- completed the live workloads within
+    // noise of this and preempted up to 36x more, profiles/r02/live_ab_scan_m20)
+    const uint32_t lim = qlen < (uint32_t)kReadyScan ? qlen : (uint32_t)kReadyScan;
+    readyPick = ready_scan(p, m, lim);
+    waitReady = readyPick < 0 && p.readyFirst >= 2 && lim >= qlen;
   }
   const bool stuck = qlen == 0 || allStalled || waitReady;
   // Voluntary quit is decided for the whole launch: a block
