@@ -67,9 +67,10 @@ class SimConfig:
     order_policy: str = "fifo"     # "fifo" | "priority"
     priority_cadence: int = 4      # priority policy: check SQ every R lane ticks
     ready_first: int = 0           # priority policy extension (reading R29): at switch-in run
-                                   # the highest-priority entry (among the first 8) every member admitted;
+                                   # the highest-priority entry (among the first ready_scan) every member admitted;
                                    # 2 = a lane whose whole queue is scanned and has no ready entry runs
                                    # nothing (waits; counts as stuck for the quit rule)
+    ready_scan: int = 64           # R29 scan window (the daemon's kReadyScan)
     stickiness: bool = True        # paper's spin-threshold policy; False = constant T
     spin_base: int = 4096          # SPEC.md:421 desk-scale defaults
     spin_step: int = 256
@@ -550,12 +551,12 @@ class Simulator:
                 # the full boostable threshold; otherwise the entry at pos waits
                 # at most spin_min
                 pick = None
-                for i, cid in enumerate(L.queue[:8]):
+                for i, cid in enumerate(L.queue[:c.ready_scan]):
                     need = R.adm[(cid, b)]
                     if all(self.ranks[q].adm.get((cid, b), 0) >= need for q in R.static[(cid, b)].members):
                         pick = i
                         break
-                L.waiting = pick is None and c.ready_first >= 2 and len(L.queue) <= 8
+                L.waiting = pick is None and c.ready_first >= 2 and len(L.queue) <= c.ready_scan
                 if L.waiting:                     # none can complete: run nothing (R29, wait mode)
                     self.ready_waits += 1
                     self._quit_check(r, b)

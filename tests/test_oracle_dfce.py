@@ -181,9 +181,9 @@ def test_bruteforce_all_orders_complete(n, k):
         _check_accounting(sim, metas, n)
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode,scan", [(1, 64), (2, 64), (2, 1)])
 @pytest.mark.parametrize("n,k", [(2, 2), (2, 3), (3, 2), (3, 3)])
-def test_bruteforce_all_orders_ready_first(n, k, mode):
+def test_bruteforce_all_orders_ready_first(n, k, mode, scan):
     """The readiness-board rule (R29: run the highest-priority entry every
     member admitted; a non-ready or non-front pick waits spin_min and is not
     boosted) keeps deadlock freedom: every (k!)^n order set completes, outputs
@@ -196,13 +196,13 @@ def test_bruteforce_all_orders_ready_first(n, k, mode):
         T = (1, 3, 64)[si % 3]
         cfg = dfce.SimConfig(spin_base=T, spin_step=max(1, T // 8), spin_min=1, spin_cap=4 * T,
                              stickiness=bool((si // 3) % 2), order_policy="priority", ready_first=mode,
-                             seed=si, **_BF_CFG)
+                             ready_scan=scan, seed=si, **_BF_CFG)
         sim, bufs = dfce.run_orders(metas, [list(o) for o in orders], cfg, seed=si)
         _check_results(sim, bufs, metas, n)
         _check_accounting(sim, metas, n)
         steered += sim.ready_picks_behind_front
         waited += sim.ready_waits
-    assert steered > 0
+    assert steered > 0 or scan == 1                      # a 1-entry window never picks behind the front
     assert (waited > 0) == (mode == 2)
 
 
