@@ -25,10 +25,13 @@ def occl_mod():
     return occl
 
 
-@pytest.mark.parametrize("policy", [1, 0])
-def test_overlapping_subcomms_random_orders(occl_mod, policy):
+@pytest.mark.parametrize("policy,ready", [(1, 2), (1, 1), (1, 0), (0, 2)])
+def test_overlapping_subcomms_random_orders(occl_mod, policy, ready):
+    """Every order policy and readiness-board mode (reading R29: 2 = wait mode,
+    1 = spinMin visits, 0 = queue front first; FIFO ignores it)."""
     n = 8
-    comms = occl_mod.local_group(n, 0, orderPolicy=policy, spinBase=256, spinStep=32, spinMin=16, **CFG)
+    comms = occl_mod.local_group(n, 0, orderPolicy=policy, readyFirst=ready, spinBase=256, spinStep=32, spinMin=16,
+                                 **CFG)
     tp_groups = [[0, 1, 2, 3], [4, 5, 6, 7]]
     pp_groups = [[i, i + 4] for i in range(4)]
     tp = occl_mod.split_group(comms, tp_groups)
