@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--policy", type=int, default=1)
     ap.add_argument("--workload", default="resnet50")
     ap.add_argument("--quit-idle-ns", type=int, default=0)
+    ap.add_argument("--gap-us", type=float, default=0.0, help="Exp-distributed gaps between submissions")
+    ap.add_argument("--per-coll", action="store_true", help="per-collective device timing of every run")
     ap.add_argument("--out", default="gpurun_out/trace_live.json")
     a = ap.parse_args()
     torch.cuda.set_device(0)
@@ -36,6 +38,12 @@ def main():
     jobs = [(c.coll_id, c.kind, c.dtype, c.count, c.root, bufs[c.coll_id]) for c in colls]
     orders = [list(range(len(colls)))] * n
     delays = [[0.0] * len(colls)] * n
+    dur = {}
+    if a.per_coll:                                     # standalone device time of each collective
+        for k, job in enumerate(jobs):
+            dur[job[0]] = sorted(harness.timed_batch(comms, [job]) for _ in range(3))[1]
+        for c in comms:
+            c.set_auto_launch(True)
     runs = []
     worst = None
     try:
@@ -44,10 +52,37 @@ def main():
             for c in comms:
                 c.trace_reset()
             before = [c.stats() for c in comms]
+            if a.gap_us:
+                delays = workloads.arrival_delays(n, len(colls), a.gap_us * 1e-6, it)
             r = harness.live_run(comms, jobs, orders, delays, timeout_s=120)
             st = {k: sum(c.stats()[k] - b[k] for c, b in zip(comms, before))
                   for k in ("launches", "quits", "preemptions", "exits", "sqeFetched")}
             row = {"run": it, "makespan_ms": r["makespan_ms"], **st}
+            if a.per_coll:
+                comms[0].quiesce(10)
+                pc = {}
+                for k, job in enumerate(jobs):
+                    cid = job[0]
+                    fet, sw, dn = [], [], []
+                    for rk in range(n):
+                        tr = comms[rk].trace(cid % 18)
+                        f = [t for t, e, c, x in tr if e == "fetch" and c == cid]
+                        if not f:
+                            continue
+                        fet.append(f[-1])
+                        s_ = [t for t, e, c, x in tr if e == "switch_in" and c == cid and t >= f[-1]]
+                        d_ = [t for t, e, c, x in tr if e == "done" and c == cid and t >= f[-1]]
+                        if s_:
+                            sw.append(s_[0])
+                        if d_:
+                            dn.append(d_[-1])
+                    if len(fet) == n and len(sw) == n and len(dn) == n:
+                        pc[cid] = {"ready_host_ms": r["ready_ms"][0][k], "last_fetch_to_last_switch_us": (max(sw) - max(fet)) / 1e3,
+                                   "last_switch_to_last_done_us": (max(dn) - max(sw)) / 1e3,
+                                   "first_switch_to_last_done_us": (max(dn) - min(sw)) / 1e3,
+                                   "standalone_us": dur[cid] * 1e3}
+                t0 = None
+                row["per_coll"] = pc
             runs.append(row)
             print(json.dumps(row), flush=True)
             if worst is None or r["makespan_ms"] > worst[0]:
