@@ -451,15 +451,19 @@ __device__ __forceinline__ void tma_load(void* smemDst, const void* gsrc, uint32
 struct TraceCtl {
   uint32_t base, idx;
 };
-__device__ __forceinline__ void trace_at(const DaemonParams& p, TraceCtl& tc, int b, uint32_t ev, int coll,
-                                         uint32_t arg) {
+__device__ __forceinline__ void trace_at_t(const DaemonParams& p, TraceCtl& tc, int b, uint32_t ev, int coll,
+                                           uint32_t arg, uint64_t t) {
   if (!p.traceCap) return;
-  const uint64_t t = globaltimer();
   const uint32_t k = tc.base + atomicAdd(&tc.idx, 1u);       // shared-memory atomic
   TraceRec* r = p.trace + (size_t)b * p.traceCap + (k % p.traceCap);
   const uint4 v = make_uint4((uint32_t)t, (uint32_t)(t >> 32), (ev << 24) | ((uint32_t)coll & 0xffffu), arg);
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(r), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
   atomicMax(&p.traceCount[b], k + 1);                          // readable while the daemon runs
+}
+__device__ __forceinline__ void trace_at(const DaemonParams& p, TraceCtl& tc, int b, uint32_t ev, int coll,
+                                         uint32_t arg) {
+  if (!p.traceCap) return;
+  trace_at_t(p, tc, b, ev, coll, arg, globaltimer());
 }
 
 // ------------------------------------------------------------------ shared control
@@ -1146,6 +1150,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   uint64_t T = sh.T, spinStart = 0;
   const uint64_t spinNs = p.spinNs;
   unsigned long long nSlices = 0, cPoll = 0;
+  uint32_t nFailed = 0;
   const long long tRun = clock64();
   trace_at(p, *m.tr, b, kEvSwitchIn, sh.curId, sh.pos);
   // commit one slice the data warps finished (in order); the downstream side of
@@ -1295,7 +1300,11 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     if (!ok) {
       cPoll += clock64() - tp;
       const uint64_t now = globaltimer();
-      if (spinStart == 0) spinStart = now;
+      if (spinStart == 0) {
+        spinStart = now;
+        trace_at(p, *m.tr, b, kEvMark, sh.curId, 30);     // first failed poll of this slice
+      }
+      ++nFailed;
       // Priority policy, "checking the SQ more frequently": a
       // collective blocked for longer than the minimal threshold yields as soon
       // as new SQEs are there, so the scheduler admits and sorts them before any
@@ -1333,6 +1342,10 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
         break;
       }
       continue;
+    }
+    if (nFailed) {
+      trace_at(p, *m.tr, b, kEvMark, nFailed > 0xffff ? 0xffff : (int)nFailed, 31);   // failed polls of this slice
+      nFailed = 0;
     }
     spinStart = 0;
     if (prim & A_DOUT) sd.cout = reinterpret_cast<char*>(peerRecv) + doutOff;
@@ -1542,7 +1555,9 @@ template <int DT, int OP>
 __device__ __forceinline__ void ll_slice(const int prim, const char* src, const char* cin, char* dst, char* cout,
                                          const int64_t nelem, const uint32_t inSeq, const uint32_t outSeq,
                                          const int tid, const int nt, const volatile uint32_t* abortGen,
-                                         const uint32_t gen, bool& ok) {
+                                         const uint32_t gen, bool& ok, uint64_t* tLine) {
+  // tLine (tracing only): [0] this thread's first line in, [1] its store of the
+  // slice's last line
   typedef typename Elem<DT>::T T;
   constexpr int PER = 8 / sizeof(T);                 // elements per line
   const bool recv = prim & A_RECV, reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
@@ -1555,6 +1570,15 @@ __device__ __forceinline__ void ll_slice(const int prim, const char* src, const 
     pay.w[0] = pay.w[1] = 0;
     const int64_t e0 = l * PER;
     if (recv) {
+      // the local operand is loaded BEFORE the line is polled: its L2 round trip
+      // overlaps the wait instead of following it (one round trip less per hop)
+      union { uint32_t w[2]; T e[PER]; } loc;
+      loc.w[0] = loc.w[1] = 0;
+      if (reduce) {
+#pragma unroll
+        for (int k = 0; k < PER; ++k)
+          if (e0 + k < nelem) loc.e[k] = ld_cg_scalar(s + e0 + k);
+      }
       uint32_t x0, f0, x1, f1;
       for (uint32_t spin = 0;; ++spin) {
         asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -1564,12 +1588,13 @@ __device__ __forceinline__ void ll_slice(const int prim, const char* src, const 
         // every line is idempotent to rewrite -- same data, same sequence number)
         if ((spin & 7) == 7 && *abortGen != gen) { ok = false; return; }
       }
+      if (tLine && l == tid) tLine[0] = globaltimer();   // trace: first line in
       pay.w[0] = x0;
       pay.w[1] = x1;
       if (reduce) {
 #pragma unroll
         for (int k = 0; k < PER; ++k)
-          if (e0 + k < nelem) pay.e[k] = sop<DT, OP>(pay.e[k], ld_cg_scalar(s + e0 + k));
+          if (e0 + k < nelem) pay.e[k] = sop<DT, OP>(pay.e[k], loc.e[k]);
       }
     } else {
 #pragma unroll
@@ -1584,6 +1609,7 @@ __device__ __forceinline__ void ll_slice(const int prim, const char* src, const 
     if (send)
       asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};"
                    :: "l"(cout + 16 * l), "r"(pay.w[0]), "r"(outSeq), "r"(pay.w[1]), "r"(outSeq) : "memory");
+    if (tLine && l == nl - 1) tLine[1] = globaltimer();
   }
 }
 
@@ -1653,9 +1679,10 @@ __device__ __forceinline__ void tail_slice(const int prim, const char* src, cons
 // on the bandwidth (TMA) path.
 __device__ __noinline__ bool ll_dispatch(int prim, int dtype, int op, const char* src, const char* cin, char* dst,
                                          char* cout, int64_t nelem, uint32_t inSeq, uint32_t outSeq, int ctid,
-                                         int cnt, const volatile uint32_t* abortGen, uint32_t gen) {
+                                         int cnt, const volatile uint32_t* abortGen, uint32_t gen, uint64_t* tLine) {
   bool ok = true;
-  OCCL_DISPATCH(dtype, op, ll_slice, prim, src, cin, dst, cout, nelem, inSeq, outSeq, ctid, cnt, abortGen, gen, ok);
+  OCCL_DISPATCH(dtype, op, ll_slice, prim, src, cin, dst, cout, nelem, inSeq, outSeq, ctid, cnt, abortGen, gen, ok,
+                tLine);
   return ok;
 }
 
@@ -1701,8 +1728,23 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
     const long long t1 = clock64();
     const int vb = tma_vec_bytes(dtype, nelem, src, dst, cout, cin);
     if (prim & A_LL) {
+      // trace (thread 0 of the compute warps): woke with the descriptor / first
+      // line in / slice stored -- the parts of an LL hop (scripts/trace_ll.py)
+      // (and the thread that stores the slice's last line -- the one the
+      // downstream's control lane polls: that store, 23, and its first line in, 24)
+      uint64_t tLine[2] = {0, 0};
+      const bool tr = p.traceCap != 0;
+      if (tr && ctid == 0) trace_at(p, pipe.tr, b, kEvMark, (int)i, 20);
       const bool ok = ll_dispatch(prim, dtype, op, src, cin, dst, cout, nelem, inSeq, outSeq, ctid, cnt,
-                                  &pipe.abortGen, gen);
+                                  &pipe.abortGen, gen, tr ? tLine : nullptr);
+      if (tr && ctid == 0) {
+        trace_at_t(p, pipe.tr, b, kEvMark, (int)i, 21, tLine[0]);
+        trace_at(p, pipe.tr, b, kEvMark, (int)i, 22);
+      }
+      if (tr && tLine[1]) {
+        trace_at_t(p, pipe.tr, b, kEvMark, (int)i, 23, tLine[1]);
+        trace_at_t(p, pipe.tr, b, kEvMark, (int)i, 24, tLine[0]);
+      }
       if (__any_sync(0xffffffffu, !ok) && lane == 0) atomicOr(&pipe.fail[i], 1u);   // before sdone's release
     } else if (!(prim & (A_COPY | A_SEND))) {
       // direct final receive: the data is already in place, nothing to move
@@ -1895,7 +1937,20 @@ __device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& 
 template <int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonParams* __restrict__ pp, int G) {
   const int lr = blockIdx.x / G;
-  const DaemonParams& p = pp[lr];
+  // The parameters live in shared memory for the launch (uploaded only while no
+  // daemon runs): a field read in a hot loop is then an LDS, not a global load
+  // that misses L1 after every gpu-scope acquire (CCTL.IVALL invalidates the SM's
+  // L1) -- the control lane's idle LL poll iteration read 4-6 fields that way
+  // and took ~1 us (scripts/trace_ll.py, profiles/r02/)
+  __shared__ __align__(16) DaemonParams sp;
+  static_assert(sizeof(DaemonParams) % 8 == 0, "DaemonParams copy granularity");
+  {
+    const uint2* src = reinterpret_cast<const uint2*>(&pp[lr]);
+    uint2* dst = reinterpret_cast<uint2*>(&sp);
+    for (int i = threadIdx.x; i < (int)(sizeof(DaemonParams) / 8); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const DaemonParams& p = sp;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Sched sh;
   __shared__ Pipe pipe;

@@ -32,7 +32,8 @@ KIND = {"allreduce": 0, "allgather": 1, "reducescatter": 2, "broadcast": 3}
 
 
 def bench_lib():
-    L = C.CDLL(os.path.join(ROOT, "paper_2303_06324_b200", "lib", "libocclbench.so"))
+    # the harness next to the product library in use (OCCL_LIB_PATH: an A/B build)
+    L = C.CDLL(os.path.join(os.path.dirname(occl.LIB_PATH), "libocclbench.so"))
     L.occlBenchLatency.restype = C.c_int
     L.occlBenchLatency.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_int,
                                    C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int, C.c_int,

@@ -39,6 +39,9 @@ def main():
     count = a.bytes // 4
     bufs = harness.buffers("allreduce", "f32", n, count, comms)
     det, mov, exe, adm = [], [], [], []
+    parts = {k: [] for k in ("wake", "line_wait", "finish", "publish", "detect_from_store", "line_from_store",
+                             "detect_from_last_store", "poll_start_to_last_store", "issue_to_next_poll_start",
+                             "polled_late", "last_store_after_first")}
     try:
         for rep in range(a.reps):
             for c in comms:
@@ -56,6 +59,35 @@ def main():
                 evs.append(tr[r][f:])
             issue = [[t for t, e, c, x in ev if e == "issue" and c == cid] for ev in evs]
             sdone = [[t for t, e, c, x in ev if e == "sdone"] for ev in evs]
+            # compute-warp marks of LL slices (20 woke, 21 first line in, 22 stored)
+            mk = {a: [[t for t, e, c, x in ev if e == "mark" and x == a] for ev in evs] for a in (20, 21, 22, 23, 24)}
+            # control lane: first failed poll of each slice (absent when the line was already there)
+            for r in range(n):
+                up = (r - 1) % n
+                for j in range(1, min(len(issue[r]), len(mk[23][up]) + 1)):
+                    parts["detect_from_last_store"].append((issue[r][j] - mk[23][up][j - 1]) / 1e3)
+                    prev = issue[r][j - 1]
+                    fp = [t for t, e, c, x in evs[r] if e == "mark" and x == 30 and prev < t <= issue[r][j]]
+                    if fp:
+                        parts["poll_start_to_last_store"].append((mk[23][up][j - 1] - fp[0]) / 1e3)
+                        parts["issue_to_next_poll_start"].append((fp[0] - prev) / 1e3)
+                    else:
+                        parts["polled_late"].append(1.0)
+                for j in range(min(len(mk[22][r]), len(mk[23][r]))):
+                    parts["last_store_after_first"].append((mk[23][r][j] - mk[22][r][j]) / 1e3)
+            for r in range(n):
+                up = (r - 1) % n
+                m = min(len(issue[r]), len(mk[20][r]), len(mk[21][r]), len(mk[22][r]), len(sdone[r]))
+                for j in range(m):
+                    parts["wake"].append((mk[20][r][j] - issue[r][j]) / 1e3)
+                    if mk[21][r][j] > 0:
+                        parts["line_wait"].append((mk[21][r][j] - mk[20][r][j]) / 1e3)
+                        parts["finish"].append((mk[22][r][j] - mk[21][r][j]) / 1e3)
+                    parts["publish"].append((sdone[r][j] - mk[22][r][j]) / 1e3)
+                    if j >= 1 and j - 1 < len(mk[22][up]):
+                        parts["detect_from_store"].append((issue[r][j] - mk[22][up][j - 1]) / 1e3)
+                        if mk[21][r][j] > 0:
+                            parts["line_from_store"].append((mk[21][r][j] - mk[22][up][j - 1]) / 1e3)
             for r in range(n):
                 up = (r - 1) % n
                 for j in range(1, min(len(issue[r]), len(sdone[up]) + 1)):
@@ -91,13 +123,22 @@ def main():
             per_rank[rk] = ev
         tmin = min(v["fetch"] for v in per_rank.values())
         per_rank = {rk: {e: round((t - tmin) / 1e3, 2) for e, t in v.items()} for rk, v in per_rank.items()}
-        res = {"bytes": a.bytes, "hops_sampled": len(det), "per_rank_last_sample_us": per_rank,
+        # the full event sequence of one sample on rank 3's lane-0 block (switch-in .. done)
+        tr3 = comms[3].trace(cid % a.grid)
+        f = max(i for i, (t, e, c, x) in enumerate(tr3) if e == "fetch" and c == cid)
+        t0 = tr3[f][0]
+        run_seq = [(round((t - t0) / 1e3, 3), e, c, x) for t, e, c, x in tr3[f:]]
+        res = {"run_sequence_rank3": run_seq, "bytes": a.bytes, "hops_sampled": len(det), "per_rank_last_sample_us": per_rank,
                "detect_us_median": statistics.median(det) if det else None,
                "detect_us_p10": sorted(det)[len(det) // 10] if det else None,
                "move_us_median": statistics.median(mov) if mov else None,
                "execute_us_median": statistics.median(exe) if exe else None,
                "fetch_to_switchin_us_median": statistics.median(adm) if adm else None,
-               "issues_per_rank": len(issue[0]), "timeline_lane0_block": timeline}
+               "issues_per_rank": len(issue[0]),
+               "hop_parts_us_median": {k: (statistics.median(v) if v else None) for k, v in parts.items()},
+               "hop_parts_n": {k: len(v) for k, v in parts.items()},
+               "hop_parts_us_p10": {k: (sorted(v)[len(v) // 10] if v else None) for k, v in parts.items()},
+               "timeline_lane0_block": timeline}
         print(json.dumps(res))
         with open(a.out, "w") as f:
             json.dump(res, f)
