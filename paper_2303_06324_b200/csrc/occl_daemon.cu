@@ -203,7 +203,8 @@ enum : int { A_RECV = 1, A_REDUCE = 2, A_COPY = 4, A_SEND = 8,
              A_DOUT = 32,   // direct send: write into the downstream's recv buffer, not its connector
              A_LL = 64,     // LL protocol: 16-B lines {data, flag, data, flag}, no release fence
              A_DREAD = 128,   // direct read: the input is the upstream's send buffer (no message)
-             A_KEEPOUT = 256 };  // direct send whose data the downstream re-reads next hop (L2 evict-last)
+             A_KEEPOUT = 256,   // direct send whose data the downstream re-reads next hop (L2 evict-last)
+             A_LLRUN = 512 };   // LL run: the compute warps move every remaining slice themselves (Pipe::llr)
 enum : int {
   P_SEND = A_SEND,
   P_RECV = A_RECV | A_COPY,
@@ -501,6 +502,39 @@ struct Sched {
   unsigned long long cycCqe, nCqe;
 };
 
+// LL run (llSpeculate == 2, DESIGN.md §LL runs): for a latency-bound (LL)
+// collective the control lane hands the compute warps the whole remaining slice
+// schedule at once; they walk it themselves -- per slice: geometry, credit,
+// poll their lines, reduce / copy / store, one named barrier, the credit to the
+// upstream -- and stop when the schedule is done or a slice has not completed
+// within limitNs.  Wire-compatible with the per-slice LL path (same lines,
+// sequence numbers and credits).  Written by the control lane before the run's
+// descriptor is published; the out fields by compute thread 0 before its warp
+// releases the descriptor (empty[]).
+struct LLStep {                 // one ring step of an LL run: primitive and segment geometry
+  uint64_t sendOff, recvOff, len;
+  int prim, pad;
+};
+struct LLRun {
+  const DaemonParams* params;   // the launch's parameters (the run is entered through ll_dispatch)
+  int blk;
+  uint64_t sendbuff, recvbuff, count, segLen, laneLo, part, E;
+  const char* llIn;
+  char* llOut;
+  const char* creditIn;   // our credit, raised by the downstream
+  char* creditOut;        // the upstream's credit, raised by us
+  uint64_t llSlot, limitNs;
+  uint64_t nsent, nrecv, creditSeen;
+  uint32_t loop, step, slc, nloops;
+  int kind, n, r, root, inplace, dtype, op, spc, nsteps, K, sys;
+  // out
+  uint64_t oNsent, oNrecv, oCreditSeen, tProg;
+  uint32_t oLoop, oStep, oSlc, nDone;
+  // in-run exchange between compute threads
+  uint64_t credit;        // thread 0's credit poll, broadcast
+  uint32_t abort[3];      // [0], [1] by slice parity: a thread's line poll timed out; [2] credit poll timed out
+};
+
 // Control -> data warp pipeline: slice descriptors in a ring of `depth` buffers.
 // full[i] completes when the control thread published ring[i]; every compute
 // warp arrives on sdone[i] when it finished its share of the slice; the
@@ -522,6 +556,8 @@ struct Pipe {
   // abortGen and clears fail[i] (after empty[i], before reusing the slot).
   uint32_t abortGen;
   uint32_t fail[kMaxDepth];
+  LLRun llr;                     // the LL run in flight (at most one: the control lane waits for it)
+  LLStep llsteps[2 * kMaxRanks]; // its per-step table (built by the compute warps at the run's start)
 };
 
 struct Smem {
@@ -810,11 +846,18 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
       trace_at(p, *m.tr, b, kEvDone, id, 0);
       cx.d.progressed = 0;
       save_dyn(g, cx.d);
-      fence_acq_rel(0);                               // gpu scope: the CQE writer's fence.sys is cumulative
-      const uint32_t old = atom_add_acq_rel(&p.complCnt[id], 1u);
-      if (old + 1 == cx.nblocks) {
+      // a one-block collective needs no completion counter: its own fence.sys
+      // orders the data (its data warps' stores, acquired through the pipe's
+      // mbarriers) before the CQE
+      bool last = cx.nblocks == 1;
+      if (!last) {
+        fence_acq_rel(0);                             // gpu scope: the CQE writer's fence.sys is cumulative
+        const uint32_t old = atom_add_acq_rel(&p.complCnt[id], 1u);
+        last = old + 1 == cx.nblocks;
+      }
+      if (last) {
         const long long tq = clock64();
-        p.complCnt[id] = 0;
+        if (cx.nblocks != 1) p.complCnt[id] = 0;
         fence_sys();                                  // the collective's data before its CQE
         if (p.cqMode == 0) {
           st_volatile_u64(&p.cqDone[id], cx.s.subSeq);  // id slot, single writer (reading R9)
@@ -1075,6 +1118,12 @@ __device__ __forceinline__ void advance(Cursor& d, int prim, int slicesPerChunk,
   }
 }
 
+// (defined after the data-warp roles: the LL-run code sits after every hot
+// loop of the bandwidth path, whose layout it would otherwise shift)
+__device__ __noinline__ int ll_run_control(const DaemonParams& p, int b, Sched& sh, const Smem& m, Pipe& pipe,
+                                           uint32_t& issued, uint32_t& committed, Cursor& dc, uint64_t& T,
+                                           unsigned long long& nSlices);
+
 // Run the collective at the front of the scheduler until it is done or preempted.
 // Everything hot lives in registers of the control thread: the static context,
 // the issue cursor `di` (runs ahead) and the committed cursor `dc`.
@@ -1115,7 +1164,7 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
   // LL speculation: recv slices go to the data warps before their lines arrived
   // (the warps poll the lines themselves); a run whose oldest issued slice does
   // not complete within the spin threshold aborts its speculative slices
-  const bool spec = ll && p.llSpeculate != 0;
+  const bool spec = ll && p.llSpeculate == 1;
   uint64_t specSince = 0;
   const bool dRead = p.directRead != 0;
   const bool keepOut = p.l2Hints >= 3;
@@ -1186,6 +1235,14 @@ __device__ __forceinline__ int run_collective(const DaemonParams& p, int b, Sche
     }
   };
   int run;
+  // LL runs for the latency-bound shape: one slice per ring step (a block whose
+  // part is one LL slice -- the LL spread of occl_host.cc gives every small
+  // collective that shape).  Longer LL schedules keep the per-slice path, whose
+  // pipe overlaps the next slice's poll with the current slice's move (an LL
+  // run moves its slices strictly one after another: 1 MiB AR 164 vs 126 us).
+  if (ll && p.llSpeculate == 2 && spc == 1 && nloops == 1) {
+    run = ll_run_control(p, b, sh, m, pipe, issued, committed, dc, T, nSlices);
+  } else
   for (;;) {
     // ---- slices the data warps moved and published: advance the committed cursor
     if (committed != issued && mbar_test(&pipe.empty[committed % D], (committed / D) & 1)) {
@@ -1686,8 +1743,18 @@ __device__ __noinline__ bool ll_dispatch(int prim, int dtype, int op, const char
   return ok;
 }
 
-__device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pipe, Stage* stages, uint64_t* tfull,
-                                          uint64_t* tempty, uint64_t* tred, const int ctid, const int cnt) {
+// The data loop's position, kept across the returns compute_main makes for LL
+// runs (see the kernel).
+struct ComputeState {
+  uint32_t j, cs, cph;                 // descriptors consumed; staging slot and its phase parity
+  unsigned long long cWait, cData, nData;   // probes
+};
+
+// Returns the pipe slot of an LL-run descriptor (its run is entered by the
+// caller; the descriptor is not yet released), or -1 at the daemon's exit.
+__device__ __noinline__ int compute_main(const DaemonParams& p, int b, Pipe& pipe, Stage* stages, uint64_t* tfull,
+                                         uint64_t* tempty, uint64_t* tred, const int ctid, const int cnt,
+                                         ComputeState& st) {
   const uint32_t D = (uint32_t)p.pipeDepth, S = (uint32_t)p.stages;
   const bool bulk = p.bulkStores != 0;
   const int lane = ctid & 31;
@@ -1695,9 +1762,9 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
   const int l2 = p.l2Hints;
   const uint64_t pol = policy_evict_first(), polKeep = policy_evict_last();
   const bool leader = ctid == 0;                       // probes
-  unsigned long long cWait = 0, cData = 0, nData = 0;
-  uint32_t cs = 0, cph = 0;                            // staging slot and its phase parity
-  for (uint32_t j = 0;; ++j) {
+  unsigned long long cWait = st.cWait, cData = st.cData, nData = st.nData;
+  uint32_t cs = st.cs, cph = st.cph;                   // staging slot and its phase parity
+  for (uint32_t j = st.j;; ++j) {
     const uint32_t i = j % D;
     const long long t0 = clock64();
     mbar_wait(&pipe.full[i], (j / D) & 1);
@@ -1715,6 +1782,11 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
     }
     prim = __shfl_sync(0xffffffffu, prim, 0);
     if (prim == P_EXIT) break;
+    if (prim & A_LLRUN) {                              // the caller runs it (ll_run_dispatch)
+      st.j = j; st.cs = cs; st.cph = cph;
+      st.cWait = cWait; st.cData = cData; st.nData = nData;
+      return (int)i;
+    }
     dtype = __shfl_sync(0xffffffffu, dtype, 0);
     op = __shfl_sync(0xffffffffu, op, 0);
     inSeq = __shfl_sync(0xffffffffu, inSeq, 0);
@@ -1806,6 +1878,7 @@ __device__ __noinline__ void compute_main(const DaemonParams& p, int b, Pipe& pi
     atomicAdd(&p.blkStats[b].cycData, cData);
     atomicAdd(&p.blkStats[b].nData, nData);
   }
+  return -1;
 }
 
 // Publisher lane (warp 2 lane 0): makes finished slices visible to the peers in
@@ -1915,6 +1988,278 @@ __device__ __noinline__ void publisher_main(const DaemonParams& p, int b, Pipe& 
     trace_at(p, pipe.tr, b, kEvPublish, k - j + 1, (uint32_t)(hv & 0xffff) | ((uint32_t)(cv & 0xffff) << 16));
     for (uint32_t q = j; q <= k; ++q) mbar_arrive(&pipe.empty[q % D]);
     j = k + 1;
+  }
+}
+
+// Named barrier of the compute warps (id 1; barrier 0 is the launch's
+// __syncthreads).  Non-aligned form: lanes leave the line loop divergently.
+__device__ __forceinline__ void bar_sync_compute(int cnt) {
+  asm volatile("barrier.sync 1, %0;" :: "r"(cnt) : "memory");
+}
+
+// Compute warps: one LL run (LLRun).  Every compute thread walks the same slice
+// schedule (the geometry is recomputed per thread -- no broadcast needed); thread
+// ctid moves lines ctid, ctid + cnt, ... of each slice.  A slice ends with one
+// named barrier; then thread 0 raises the upstream's credit.  A line not there
+// within limitNs of its slice's start aborts the run: every thread leaves after
+// the slice's barrier, so the reported cursor is the first incomplete slice (its
+// partly sent lines are rewritten identically when it is redone).
+// The step table of an LL run: step t's primitive and segment geometry (PAPER.md
+// ring schedule, step_prim / seg_geom), built once per run by compute thread t
+// -- per slice only a table lookup and the slice's offset remain on the chain
+// between two hops (computing the geometry per slice took ~1.2 us of it).
+__device__ __noinline__ void ll_steps(const LLRun& L, LLStep* tab, int ctid, int cnt) {
+  for (int t = ctid; t < L.nsteps; t += cnt) {
+    int prim, seg;
+    step_prim(L.kind, L.n, L.r, L.root, t, L.inplace != 0, prim, seg);
+    uint64_t sendOff, recvOff, len;
+    seg_geom(L.kind, L.n, L.r, L.count, L.segLen, seg, sendOff, recvOff, len);
+    tab[t].sendOff = sendOff;
+    tab[t].recvOff = recvOff;
+    tab[t].len = len;
+    tab[t].prim = prim;
+  }
+}
+
+template <int DT, int OP>
+__device__ __forceinline__ void ll_run(const DaemonParams& p, LLRun& L, Pipe& pipe, int b, const int ctid,
+                                       const int cnt) {
+  typedef typename Elem<DT>::T T;
+  constexpr int PER = 8 / sizeof(T);                 // elements per line
+  const uint64_t limitNs = L.limitNs;
+  const int K = L.K, spc = L.spc, nsteps = L.nsteps, sys = L.sys;
+  const uint32_t nloops = L.nloops;
+  const uint64_t laneLo = L.laneLo, part = L.part, E = L.E, llSlot = L.llSlot;
+  const T* sendbuff = reinterpret_cast<const T*>(L.sendbuff);
+  T* recvbuff = reinterpret_cast<T*>(L.recvbuff);
+  const char* llIn = L.llIn;
+  char* llOut = L.llOut;
+  Cursor c{L.loop, L.step, L.slc, L.nsent, L.nrecv};
+  uint32_t slotIn = (uint32_t)(c.nrecv % (uint64_t)K), slotOut = (uint32_t)(c.nsent % (uint64_t)K);
+  uint64_t creditSeen = L.creditSeen;
+  volatile uint32_t* abortf = L.abort;                // [0], [1]: line timeouts by slice parity; [2]: credit timeout
+  uint32_t nDone = 0;
+  const bool tr = p.traceCap != 0 && ctid == 0;
+  const LLStep* tab = pipe.llsteps;
+  ll_steps(L, pipe.llsteps, ctid, cnt);
+  bar_sync_compute(cnt);
+  while (c.loop < nloops) {
+    const uint32_t par = nDone & 1;
+    if (ctid == 0) abortf[par ^ 1] = 0;              // the next slice's flag (this one's is clear: we got here)
+    const uint64_t t0 = globaltimer();
+    if (tr) trace_at_t(p, pipe.tr, b, kEvMark, (int)c.step, 40, t0);
+    const LLStep& S = tab[c.step];
+    const int prim = S.prim;
+    uint64_t laneHi = laneLo + part;
+    if (laneHi > S.len) laneHi = S.len;
+    const uint64_t lo = laneLo + ((uint64_t)c.loop * spc + c.slc) * E;
+    uint64_t hi = lo + E;
+    if (hi > laneHi) hi = laneHi;
+    const int64_t nelem = hi > lo ? (int64_t)(hi - lo) : 0;
+    const T* src = sendbuff + (S.sendOff + lo);
+    T* dst = recvbuff + (S.recvOff + lo);
+    const char* cin = llIn + slotIn * llSlot;
+    char* cout = llOut + slotOut * llSlot;
+    const bool recv = prim & A_RECV, reduce = prim & A_REDUCE, copy = prim & A_COPY, send = prim & A_SEND;
+    if (tr) trace_at(p, pipe.tr, b, kEvMark, (int)c.step, 42);
+    if (send && c.nsent - creditSeen >= (uint64_t)K) {
+      // flow control: thread 0 polls the downstream's credit, the barrier broadcasts it
+      if (ctid == 0) {
+        uint64_t cr;
+        for (;;) {
+          cr = ld_acquire(L.creditIn, sys);
+          if (c.nsent - cr < (uint64_t)K) break;
+          if (globaltimer() - t0 > limitNs) { abortf[2] = 1; break; }
+        }
+        *reinterpret_cast<volatile uint64_t*>(&L.credit) = cr;
+      }
+      bar_sync_compute(cnt);
+      if (tr) trace_at(p, pipe.tr, b, kEvMark, (int)c.step, 43);
+      if (abortf[2]) break;                            // sticky for the run: every thread sees it
+      const uint64_t cr = *reinterpret_cast<volatile uint64_t*>(&L.credit);
+      if (cr > creditSeen) creditSeen = cr;
+    }
+    // thread 0 reads the downstream's credit once per sending slice, early (the
+    // load is in flight while the lines are polled) and hands it to every thread
+    // through the slice's barrier: the blocking credit wait above becomes rare
+    uint64_t crEarly = 0;
+    if (send && ctid == 0) crEarly = ld_relaxed(L.creditIn, sys);
+    const uint32_t inSeq = (uint32_t)(c.nrecv + 1), outSeq = (uint32_t)(c.nsent + 1);
+    const int64_t lines = (nelem + PER - 1) / PER;
+    const int64_t nl = lines ? lines : 1;              // an empty message still carries one token line
+    for (int64_t l = ctid; l < nl; l += cnt) {
+      union { uint32_t w[2]; T e[PER]; } pay, loc;
+      pay.w[0] = pay.w[1] = 0;
+      const int64_t e0 = l * PER;
+      if (recv) {
+        // the local operand is loaded before the line is polled (its round trip
+        // overlaps the wait)
+        loc.w[0] = loc.w[1] = 0;
+        if (reduce) {
+#pragma unroll
+          for (int k = 0; k < PER; ++k)
+            if (e0 + k < nelem) loc.e[k] = ld_cg_scalar(src + e0 + k);
+        }
+        uint32_t x0, f0, x1, f1;
+        bool got = true;
+        uint32_t spin = 0;
+        for (;; ++spin) {
+          asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(x0), "=r"(f0), "=r"(x1), "=r"(f1) : "l"(cin + 16 * l) : "memory");
+          if (f0 == inSeq && f1 == inSeq) break;
+          if ((spin & 7) == 7 && (abortf[par] || globaltimer() - t0 > limitNs)) {
+            abortf[par] = 1;
+            got = false;
+            break;
+          }
+        }
+        if (!got) break;
+        if (tr && l == ctid) trace_at(p, pipe.tr, b, kEvMark, (int)spin, 44);
+        pay.w[0] = x0;
+        pay.w[1] = x1;
+        if (reduce) {
+#pragma unroll
+          for (int k = 0; k < PER; ++k)
+            if (e0 + k < nelem) pay.e[k] = sop<DT, OP>(pay.e[k], loc.e[k]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < PER; ++k)
+          if (e0 + k < nelem) pay.e[k] = ld_cg_scalar(src + e0 + k);
+      }
+      if (copy) {
+#pragma unroll
+        for (int k = 0; k < PER; ++k)
+          if (e0 + k < nelem) dst[e0 + k] = pay.e[k];
+      }
+      if (send)
+        asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};"
+                     :: "l"(cout + 16 * l), "r"(pay.w[0]), "r"(outSeq), "r"(pay.w[1]), "r"(outSeq) : "memory");
+    }
+    if (tr) trace_at(p, pipe.tr, b, kEvMark, (int)c.step, 45);
+    if (send && ctid == 0) *reinterpret_cast<volatile uint64_t*>(&L.credit) = crEarly;
+    bar_sync_compute(cnt);
+    if (abortf[par]) break;
+    if (send) {                                        // credits are monotonic: a later value is as good
+      const uint64_t cr = *reinterpret_cast<volatile uint64_t*>(&L.credit);
+      if (cr > creditSeen) creditSeen = cr;
+    }
+    if (ctid == 0) {
+      // LL credits follow loads that already returned their values: no fence
+      if (recv) red_max_relaxed(L.creditOut, c.nrecv + 1, sys);
+      L.tProg = globaltimer();
+      if (tr) trace_at(p, pipe.tr, b, kEvMark, (int)c.step, 41);
+    }
+    if (recv && ++slotIn == (uint32_t)K) slotIn = 0;
+    if (send && ++slotOut == (uint32_t)K) slotOut = 0;
+    advance(c, prim, spc, nsteps);
+    ++nDone;
+  }
+  if (ctid == 0) {
+    L.oLoop = c.loop; L.oStep = c.step; L.oSlc = c.slc;
+    L.oNsent = c.nsent; L.oNrecv = c.nrecv; L.oCreditSeen = creditSeen;
+    L.nDone = nDone;
+  }
+}
+
+
+// Entered from the kernel's top level, not from compute_main: as a callee of the
+// data loop its registers made compute_main spill (176 B) and slowed every
+// Simple-protocol slice (1 MiB AR 165 vs 121 us).
+__device__ __noinline__ void ll_run_dispatch(const DaemonParams& p, Pipe& pipe, int b, int ctid, int cnt) {
+  LLRun& L = pipe.llr;
+  OCCL_DISPATCH(L.dtype, L.op, ll_run, p, L, pipe, b, ctid, cnt);
+}
+
+// Control lane side of an LL run (LLRun; llSpeculate == 2).  One descriptor
+// hands the compute warps the collective's remaining slices; the lane waits for
+// the run, takes over the cursor it reports and decides as the per-slice path
+// does: done, or -- no slice completed for T spins -- preempted.  Under the
+// priority policy a run gives up after spinMin spins at most, so that the lane
+// can look at the SQ (yield to new SQEs) and re-issue the run
+// when nothing new is there.  Returns RUN_DONE / RUN_PREEMPT.
+__device__ __noinline__ int ll_run_control(const DaemonParams& p, int b, Sched& sh, const Smem& m, Pipe& pipe,
+                                           uint32_t& issued, uint32_t& committed, Cursor& dc, uint64_t& T,
+                                           unsigned long long& nSlices) {
+  const uint32_t D = (uint32_t)p.pipeDepth;
+  CtxSlot& cx = m.cache[sh.way];
+  const RingDesc& R = p.rings[cx.sub];
+  const size_t cb = (size_t)sh.curId * p.G + b;
+  const int K = p.K;
+  const uint64_t llSlot = 2ull * p.llSliceBytes;
+  LLRun& L = pipe.llr;
+  // the downstream's credit as it stands (relaxed; its latency overlaps the stores
+  // below): without it the run's first send would wait for a credit poll
+  const uint64_t cr0 = ld_relaxed(p.flagsLocal + cb * kFlagStride + 128, p.sysScope);
+  L.params = &p;
+  L.blk = b;
+  L.sendbuff = cx.s.sendbuff; L.recvbuff = cx.s.recvbuff; L.count = cx.s.count; L.segLen = cx.s.segLen;
+  L.part = cx.s.part;
+  L.laneLo = (uint64_t)cx.lane * cx.s.part;
+  L.E = p.llSliceBytes / elem_size(cx.d.dtype);
+  L.llIn = p.llLocal + cb * K * llSlot;
+  L.llOut = R.llNext + cb * K * llSlot;
+  L.creditIn = p.flagsLocal + cb * kFlagStride + 128;
+  L.creditOut = R.flagsPrev + cb * kFlagStride + 128;
+  L.llSlot = llSlot;
+  L.nloops = cx.d.nloops;
+  L.kind = cx.d.kind; L.n = R.nranks; L.r = R.rank; L.root = cx.root;
+  L.inplace = cx.s.sendbuff == cx.s.recvbuff; L.dtype = cx.d.dtype; L.op = (int)cx.op; L.spc = (int)cx.spc;
+  L.nsteps = cx.nsteps; L.K = K; L.sys = p.sysScope;
+  L.creditSeen = cr0;
+  const uint64_t spinNs = p.spinNs;
+  const bool yieldable = p.orderPolicy == 1 && p.sqYieldNs != 0;
+  uint64_t tProg = globaltimer();                      // last progress (or the run's start)
+  for (;;) {
+    const uint64_t hard = T * spinNs;
+    uint64_t lim = hard;
+    if (yieldable && (uint64_t)p.spinMin * spinNs < lim) lim = (uint64_t)p.spinMin * spinNs;
+    L.limitNs = lim;
+    L.loop = dc.loop; L.step = dc.step; L.slc = dc.slc; L.nsent = dc.nsent; L.nrecv = dc.nrecv;
+    L.abort[0] = L.abort[1] = L.abort[2] = 0;
+    L.nDone = 0;
+    L.tProg = 0;
+    SliceDesc& sd = pipe.ring[issued % D];
+    sd.prim = A_LL | A_LLRUN;
+    sd.dtype = cx.d.dtype; sd.op = (int)cx.op; sd.nelem = 0;
+    sd.src = nullptr; sd.cin = nullptr; sd.dst = nullptr; sd.cout = nullptr;
+    sd.gen = pipe.abortGen;
+    mbar_arrive(&pipe.full[issued % D]);             // committed == issued: the slot is free
+    trace_at(p, *m.tr, b, kEvIssue, sh.curId, 0xfff00000u);
+    ++issued;
+    mbar_wait(&pipe.empty[committed % D], (committed / D) & 1);
+    ++committed;
+    const uint32_t nd = L.nDone;
+    dc.loop = L.oLoop; dc.step = L.oStep; dc.slc = L.oSlc; dc.nsent = L.oNsent; dc.nrecv = L.oNrecv;
+    L.creditSeen = L.oCreditSeen;
+    if (nd) {
+      nSlices += nd;
+      tProg = L.tProg;
+      if (p.stickiness && sh.boostOk) {               // raise the threshold, once per run
+        T *= p.spinBoost;
+        if (T > p.spinCap) T = p.spinCap;
+      }
+      m.tq[sh.pos] &= 0xffffu;                        // progressed: not stalled
+    }
+    if (dc.loop >= cx.d.nloops) return RUN_DONE;
+    const uint64_t now = globaltimer();
+    if (now - tProg > T * spinNs) return RUN_PREEMPT;  // two-phase blocking: preempt
+    if (yieldable) {
+      // the run gave up after spinMin spins: new SQEs? (as in the per-slice path)
+      const uint64_t tail = ld_acquire(p.mirrorTail, 0);
+      if (tail > sh.cursor) return RUN_PREEMPT;
+      unsigned long long* lastHost = reinterpret_cast<unsigned long long*>(p.mirrorTail + 3);
+      const unsigned long long lh = *reinterpret_cast<volatile unsigned long long*>(lastHost);
+      if (now - lh > p.sqYieldNs && atomicCAS(lastHost, lh, (unsigned long long)now) == lh) {
+        uint32_t stamp;
+        asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(stamp) : "l"(p.sq[tail % p.sqDepth].c[0])
+                     : "memory");
+        if (stamp == (uint32_t)(tail + 1)) {
+          sh.needHostPoll = 1;
+          return RUN_PREEMPT;
+        }
+      }
+    }
   }
 }
 
@@ -2033,7 +2378,21 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
     else if (tid == 64) publisher_main(p, b, pipe, stages, tfull, tempty, tred);
     return;
   }
-  compute_main(p, b, pipe, stages, tfull, tempty, tred, tid - 32 * kRoleWarps, nComputeWarps * 32);
+  // compute warps: the data loop, left for each LL run (entered here, at the top
+  // level, so that the run's registers do not constrain the data loop's)
+  ComputeState cst{0, 0, 0, 0, 0, 0};
+  const int ctid = tid - 32 * kRoleWarps, cnt = nComputeWarps * 32;
+  for (;;) {
+    const int i = compute_main(p, b, pipe, stages, tfull, tempty, tred, ctid, cnt, cst);
+    if (i < 0) break;
+    ll_run_dispatch(p, pipe, b, ctid, cnt);
+    __syncwarp();
+    if ((ctid & 31) == 0) {
+      mbar_arrive(&pipe.sdone[i]);
+      mbar_arrive(&pipe.empty[i]);                     // this warp is done with ring[i] too
+    }
+    ++cst.j;
+  }
 }
 
 extern "C" size_t occl_internal_daemon_smem(int maxColl, int cacheWays, int stages) {

@@ -388,6 +388,7 @@ occlResult_t validate_config(const occlConfig_t& c) {
   if (c.priorityCadence < 1) return occlInvalidArgument;
   if (c.stallLimit < 1) return occlInvalidArgument;
   if (c.pipeDepth < 1 || c.pipeDepth > 8) return occlInvalidArgument;
+  if (c.llSpeculate < 0 || c.llSpeculate > 2) return occlInvalidArgument;
   if (c.prefetchSlices != 0) return occlInvalidArgument;       // reserved (the L2 prefetch was removed)
   if (c.readyFirst < 0 || c.readyFirst > 2) return occlInvalidArgument;
   if (c.stagingTiles < 1 || c.stagingTiles > 6) return occlInvalidArgument;
@@ -607,7 +608,7 @@ occlResult_t occlConfigDefault(occlConfig_t* c) {
   c->blocksPerSM = 1;
   c->l2Hints = 2;
   c->sqYieldNs = 20'000;
-  c->llSpeculate = 0;
+  c->llSpeculate = 2;
   c->readyFirst = 2;
   return occlSuccess;
 }

@@ -104,7 +104,7 @@ def main():
     ap.add_argument("--ll-slice", type=int, default=0)
     ap.add_argument("--min-block", type=int, default=0)
     ap.add_argument("--cq-mode", type=int, default=0)
-    ap.add_argument("--ll-spec", type=int, default=0)
+    ap.add_argument("--ll-spec", type=int, default=-1, help="llSpeculate (0 per-slice LL, 1 speculation, 2 LL runs)")
     ap.add_argument("--tag", default="")
     ap.add_argument("--out", default="gpurun_out/latency_split")
     a = ap.parse_args()
@@ -119,8 +119,8 @@ def main():
         extra["minBlockBytes"] = a.min_block
     if a.cq_mode:
         extra["cqMode"] = a.cq_mode
-    if a.ll_spec:
-        extra["llSpeculate"] = 1
+    if a.ll_spec >= 0:
+        extra["llSpeculate"] = a.ll_spec
     L = bench_lib()
     rows = []
     # e2e samples without tracing; the split from a second, traced ring (the trace's
