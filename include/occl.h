@@ -128,11 +128,15 @@ typedef struct {
   uint64_t sqYieldNs;     /* priority policy: a collective blocked on a peer for >= spinMin spins yields to
                              newly submitted SQEs; its rank polls the host SQ for them at most once per
                              sqYieldNs (0 = never: new SQEs are seen only between runs) */
-  int llSpeculate;        /* 1 = LL slices are handed to the data warps before their lines arrived: the
-                             warps poll the lines themselves (one L2 round trip per hop less); a slice
-                             whose lines do not come within the spin threshold is aborted and redone
-                             later (LL lines are idempotent to rewrite).  0 = the control lane polls the
-                             slice's last line first */
+  int llSpeculate;        /* LL slice driving (DESIGN.md §LL runs).  2 (default) = LL runs: a collective
+                             whose blocks move one LL slice per ring step is handed to the data warps
+                             as ONE descriptor; they walk its whole slice schedule, polling their own
+                             lines, and stop when a slice's lines do not come within the spin threshold
+                             (the control lane resumes from the reported cursor); longer LL schedules
+                             use mode 0.  1 = LL slices are handed to the data warps one by one before
+                             their lines arrived (abortable speculation).  0 = the control lane polls
+                             each slice's last line, then issues it.  All modes are wire-compatible.
+                             Other values: occlInvalidArgument */
   int readyFirst;         /* priority policy: 1/2 = run the highest-priority collective that EVERY member
                              rank has admitted (each rank publishes its admissions on a readiness
                              board in its flags; R29); a collective not yet admitted

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Small end-to-end run of the daemon for compute-sanitizer (memcheck /
 synccheck / racecheck): every kind, Simple and LL (with and without LL
-speculation), direct mode on and off, a sub-communicator, the TMA SQ fetch and
+speculation, and as LL runs), direct mode on and off, a sub-communicator, the TMA SQ fetch and
 the readiness board, checked bit-exactly against the oracle.  Sizes are tiny so
 the instrumented persistent kernel finishes in minutes.
 
@@ -28,7 +28,9 @@ def main():
     # (direct mode, LL limit, LL speculation): Simple + LL with direct mode, Simple-only
     # connector path, LL with speculation (abortable data-warp polling); the default
     # priority policy with the readiness board throughout
-    for direct, llmax, spec in [(1, 64 << 10, 0), (0, 0, 0), (1, 64 << 10, 1)]:
+    # (and LL runs, llSpeculate = 2: data warps walking a whole slice schedule with
+    # a named barrier per slice)
+    for direct, llmax, spec in [(1, 64 << 10, 0), (0, 0, 0), (1, 64 << 10, 1), (1, 64 << 10, 2)]:
         comms = occl.local_group(n, 0, gridBlocks=2, maxColl=8, sliceBytes=16 << 10, stagingTiles=2,
                                  directMode=direct, llMaxBytes=llmax, llSpeculate=spec, quitIdleNs=500_000)
         try:

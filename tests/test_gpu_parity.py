@@ -59,14 +59,15 @@ def test_generator_matches_numpy(occl_mod):
 @pytest.mark.parametrize("kind", ring.KINDS)
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
-@pytest.mark.parametrize("proto", ["ll", "ll-spec", "simple"])
+@pytest.mark.parametrize("proto", ["ll", "ll-spec", "ll-run", "simple"])
 def test_parity_small(occl_mod, kind, dtype, n, proto):
     """LL (flags inside 16-B lines) for small per-block parts -- with the data
-    warps polling the lines themselves (ll-spec, cfg.llSpeculate) or after the
-    control lane saw the slice's last line -- and Simple (head / credit flags +
-    release fence) when LL is disabled."""
-    comms = group(occl_mod, n, llMaxBytes=0 if proto == "simple" else (64 << 10),
-                  llSpeculate=int(proto == "ll-spec"))
+    warps polling the lines themselves (ll-spec, cfg.llSpeculate = 1), after the
+    control lane saw the slice's last line (ll, 0), or walking the whole slice
+    schedule as an LL run (ll-run, 2, the default) -- and Simple (head / credit
+    flags + release fence) when LL is disabled."""
+    mode = {"ll": 0, "ll-spec": 1, "ll-run": 2, "simple": 2}[proto]
+    comms = group(occl_mod, n, llMaxBytes=0 if proto == "simple" else (64 << 10), llSpeculate=mode)
     for ci, count in enumerate([1, 7, 256, 1000, 4099, 65536]):
         root = (ci + 1) % n
         seed = 1000 + ci
@@ -88,7 +89,7 @@ def test_parity_inplace(occl_mod, kind, n):
 
 
 @pytest.mark.parametrize("n", [2, 4, 8])
-@pytest.mark.parametrize("llmax,spec", [(0, 0), (1 << 20, 0), (1 << 20, 1)])
+@pytest.mark.parametrize("llmax,spec", [(0, 0), (1 << 20, 0), (1 << 20, 1), (1 << 20, 2)])
 def test_parity_1mib_multiblock(occl_mod, n, llmax, spec):
     """1 Mi elements: many loops and slices per block, ragged tail, all blocks;
     Simple, and LL forced for every size (many LL slices and loops), with and

@@ -108,6 +108,32 @@ def test_ll_speculation_random_orders(occl_mod, T):
         occl_mod.destroy_group(comms)
 
 
+@pytest.mark.parametrize("T", [1, 8, 4096])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_ll_runs_random_orders(occl_mod, T, policy):
+    """LL runs (cfg.llSpeculate = 2): the compute warps walk a latency-bound
+    collective's whole slice schedule and stop when a slice's lines do not come
+    within the spin threshold; the control lane takes over the reported cursor
+    (preempted runs resume there; partly sent lines are rewritten identically).
+    Misordered submissions, tiny thresholds, FIFO and priority policies: results
+    bit-exact, and at T = 1 runs are preempted."""
+    comms = occl_mod.local_group(8, 0, **BASE, llSpeculate=2, orderPolicy=policy, spinBase=T, spinStep=1,
+                                 spinMin=1, spinCap=max(T, 4 * T))
+    try:
+        rng = random.Random(2000 + T + 7 * policy)
+        kinds = ["allreduce", "allgather", "reducescatter", "broadcast"]
+        colls = [workloads.Coll(i, kinds[i % 4], ["f32", "bf16", "i32"][i % 3], rng.randint(1, 6_000),
+                                root=rng.randrange(8)) for i in range(8)]
+        for it in range(4):
+            orders = [rng.sample(range(8), 8) for _ in range(8)]
+            _run_orders(comms, colls, orders, seed=500 * T + it + 50 * policy)
+        pre = sum(c.stats()["preemptions"] for c in comms)
+        if T == 1 and policy == 0:
+            assert pre > 0
+    finally:
+        occl_mod.destroy_group(comms)
+
+
 def test_deadlock_campaign_small(occl_mod):
     """PAPER.md:736-739 at n=8: ARs of 256 B..1 MiB in independent random per-rank
     orders; every trial must complete (0 timeouts) and match the oracle."""
