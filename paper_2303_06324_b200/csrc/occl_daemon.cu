@@ -2023,7 +2023,7 @@ __device__ __noinline__ void ll_steps(const LLRun& L, LLStep* tab, int ctid, int
 
 template <int DT, int OP>
 __device__ __forceinline__ void ll_run(const DaemonParams& p, LLRun& L, Pipe& pipe, int b, const int ctid,
-                                       const int cnt) {
+                                       int cnt) {
   typedef typename Elem<DT>::T T;
   constexpr int PER = 8 / sizeof(T);                 // elements per line
   const uint64_t limitNs = L.limitNs;
@@ -2041,6 +2041,16 @@ __device__ __forceinline__ void ll_run(const DaemonParams& p, LLRun& L, Pipe& pi
   uint32_t nDone = 0;
   const bool tr = p.traceCap != 0 && ctid == 0;
   const LLStep* tab = pipe.llsteps;
+  // only the warps a slice has lines for take part (a 4 KiB all-reduce at 8
+  // ranks: 64 lines, 2 of 16 warps): the others leave at once, and the per-slice
+  // barrier waits for fewer warps
+  {
+    const uint64_t maxElem = part < E ? part : E;
+    int nw = (int)(((maxElem * sizeof(T) + 7) / 8 + 31) / 32);
+    if (nw < 1) nw = 1;
+    if (nw * 32 < cnt) cnt = nw * 32;
+    if (ctid >= cnt) return;
+  }
   ll_steps(L, pipe.llsteps, ctid, cnt);
   bar_sync_compute(cnt);
   while (c.loop < nloops) {
