@@ -78,6 +78,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--check", action="store_true", help="sampled oracle check of the timed output")
+    ap.add_argument("--no-latency", action="store_true", help="N=1: skip the small-message latency key")
     return ap.parse_args()
 
 
@@ -491,11 +492,54 @@ def run_single(args, world, prank, local, dist):
         co = conn_only_variant(args, dev, sends, recvs, size, peaks)
         co["vs_direct_mode"] = co["value"] / value
         line["connector_only"] = co
+    if world == 1 and not args.no_latency:
+        line["latency"] = small_message_latency(dev)
     if prank == 0:
         print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def small_message_latency(dev, sizes=(4096, 65536, 1 << 20), reps=50):
+    """End-to-end latency of single all-reduces (fp32, 8 virtual ranks, live
+    daemon, library defaults): native per-rank threads submit at one instant and
+    occlWait through the C-ABI (libocclbench.so); sample = max(done) -
+    min(submit); median and p10/p90 of `reps` (the metric's "latency vs size",
+    scripts/latency_split.py has the per-size split)."""
+    import ctypes as C
+    import statistics
+    from paper_2303_06324_b200 import harness, occl
+    L = C.CDLL(os.path.join(os.path.dirname(occl.LIB_PATH), "libocclbench.so"))
+    L.occlBenchLatency.restype = C.c_int
+    L.occlBenchLatency.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int, C.c_int,
+                                   C.POINTER(C.c_double)]
+    n = 8
+    comms = harness.ring(n, dev, gridBlocks=18, maxColl=16, quitIdleNs=10_000_000_000)
+    out = {"ranks": n, "kind": "allreduce", "dtype": "f32", "unit": "us", "reps": reps,
+           "definition": "max(done) - min(submit), native per-rank threads through the C-ABI"}
+    try:
+        hs = (C.c_void_p * n)(*[c.h if isinstance(c.h, int) else c.h.value for c in comms])
+        for S in sizes:
+            count = S // 4
+            bufs = harness.buffers("allreduce", "f32", n, count, comms)
+            ss = (C.c_void_p * n)(*[bufs[r][0].data_ptr() for r in range(n)])
+            rs = (C.c_void_p * n)(*[bufs[r][1].data_ptr() for r in range(n)])
+            res = (C.c_double * reps)()
+            for k in (5, reps):                          # warm-up, then the sample
+                rc = L.occlBenchLatency(hs, n, 0, count, occl.DTYPE["f32"], 0, 0, ss, rs, 1, k, res)
+                if rc != 0:
+                    raise RuntimeError(f"occlBenchLatency rc={rc}")
+            lat = sorted(res[i] / 1e3 for i in range(reps))
+            out[f"{S}B"] = {"median": statistics.median(lat), "p10": lat[reps // 10], "p90": lat[(9 * reps) // 10]}
+            del bufs
+    finally:
+        for c in comms:
+            c.exit()
+        comms[0].quiesce(60)
+        occl.destroy_group(comms)
+    return out
 
 
 def conn_only_variant(args, dev, sends, recvs, size, peaks):

@@ -41,7 +41,8 @@ def main():
     det, mov, exe, adm = [], [], [], []
     parts = {k: [] for k in ("wake", "line_wait", "finish", "publish", "detect_from_store", "line_from_store",
                              "detect_from_last_store", "poll_start_to_last_store", "issue_to_next_poll_start",
-                             "polled_late", "last_store_after_first")}
+                             "polled_late", "last_store_after_first", "run_slice_period", "run_start_to_done",
+                             "run_stored_to_done", "run_upstream_stored_to_start")}
     try:
         for rep in range(a.reps):
             for c in comms:
@@ -59,6 +60,19 @@ def main():
                 evs.append(tr[r][f:])
             issue = [[t for t, e, c, x in ev if e == "issue" and c == cid] for ev in evs]
             sdone = [[t for t, e, c, x in ev if e == "sdone"] for ev in evs]
+            # LL runs (llSpeculate = 2): thread 0's marks per slice -- 40 start, 44 first line
+            # in, 45 stores issued, 41 slice done (after the barrier and the credit)
+            lr = {a: [[t for t, e, c, x in ev if e == "mark" and x == a] for ev in evs] for a in (40, 41, 44, 45)}
+            for r in range(n):
+                up = (r - 1) % n
+                for j in range(1, len(lr[41][r])):
+                    parts["run_slice_period"].append((lr[41][r][j] - lr[41][r][j - 1]) / 1e3)
+                m = min(len(lr[40][r]), len(lr[41][r]), len(lr[45][r]))
+                for j in range(m):
+                    parts["run_start_to_done"].append((lr[41][r][j] - lr[40][r][j]) / 1e3)
+                    parts["run_stored_to_done"].append((lr[41][r][j] - lr[45][r][j]) / 1e3)
+                for j in range(1, min(len(lr[40][r]), len(lr[45][up]) + 1)):
+                    parts["run_upstream_stored_to_start"].append((lr[40][r][j] - lr[45][up][j - 1]) / 1e3)
             # compute-warp marks of LL slices (20 woke, 21 first line in, 22 stored)
             mk = {a: [[t for t, e, c, x in ev if e == "mark" and x == a] for ev in evs] for a in (20, 21, 22, 23, 24)}
             # control lane: first failed poll of each slice (absent when the line was already there)
