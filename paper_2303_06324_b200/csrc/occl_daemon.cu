@@ -500,6 +500,7 @@ struct Sched {
   unsigned long long cycRun, cycPoll, cycAcqFence, cycRelFence, nCommit;   // probes
   unsigned long long cycCtxLoad, nCtxLoad, cycCtxSave, nCtxSave;
   unsigned long long cycCqe, nCqe;
+  unsigned long long idlePolls;
 };
 
 // LL run (llSpeculate == 2, DESIGN.md §LL runs): for a latency-bound (LL)
@@ -1090,7 +1091,7 @@ __device__ __noinline__ int schedule(const DaemonParams& p, int b, Sched& sh, co
     }
     cmd = CMD_RUN;
   } else {
-    p.blkStats[b].idlePolls++;
+    ++sh.idlePolls;                                  // (a global ++ here cost an L2 round trip per idle round)
     if (p.idleSleepNs) __nanosleep(p.idleSleepNs);
   }
   if (cmd == CMD_EXIT) {                             // persist what survives the quit
@@ -1451,6 +1452,7 @@ __device__ __noinline__ void control_main(const DaemonParams& p, int b, Sched& s
   bst.nCtxSave += sh.nCtxSave;
   bst.cycCqe += sh.cycCqe;
   bst.nCqe += sh.nCqe;
+  bst.idlePolls += sh.idlePolls;
   // release the data warps (the pipe is drained after every run)
   pipe.ring[issued % D].prim = P_EXIT;
   mbar_arrive(&pipe.full[issued % D]);
@@ -2350,6 +2352,7 @@ __global__ void __launch_bounds__(MAXT, MINB) occl_daemon_kernel(const DaemonPar
     sh.cycRun = sh.cycPoll = sh.cycAcqFence = sh.cycRelFence = sh.nCommit = 0;
     sh.cycCtxLoad = sh.nCtxLoad = sh.cycCtxSave = sh.nCtxSave = 0;
     sh.cycCqe = sh.nCqe = 0;
+    sh.idlePolls = 0;
     for (uint32_t i = 0; i < sh.qlen; ++i) {
       m.tq[i] = p.tqSave[(size_t)b * p.maxColl + i];
       const int c = (int)(m.tq[i] & 0xffffu);
