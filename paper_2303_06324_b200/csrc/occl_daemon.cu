@@ -517,8 +517,6 @@ struct LLStep {                 // one ring step of an LL run: primitive and seg
   int prim, pad;
 };
 struct LLRun {
-  const DaemonParams* params;   // the launch's parameters (the run is entered through ll_dispatch)
-  int blk;
   uint64_t sendbuff, recvbuff, count, segLen, laneLo, part, E;
   const char* llIn;
   char* llOut;
@@ -2203,8 +2201,6 @@ __device__ __noinline__ int ll_run_control(const DaemonParams& p, int b, Sched& 
   // the downstream's credit as it stands (relaxed; its latency overlaps the stores
   // below): without it the run's first send would wait for a credit poll
   const uint64_t cr0 = ld_relaxed(p.flagsLocal + cb * kFlagStride + 128, p.sysScope);
-  L.params = &p;
-  L.blk = b;
   L.sendbuff = cx.s.sendbuff; L.recvbuff = cx.s.recvbuff; L.count = cx.s.count; L.segLen = cx.s.segLen;
   L.part = cx.s.part;
   L.laneLo = (uint64_t)cx.lane * cx.s.part;
