@@ -582,7 +582,7 @@ __device__ __forceinline__ void save_dyn(CtxSlot* g, const DynCtx& d) {
 // Admit an SQE into this block's task queue: write the static context and reset
 // the dynamic cursor (keeping the connector sequence numbers).
 __device__ __noinline__ void admit(const DaemonParams& p, int b, int lane, Sched& sh, const Smem& m, const Sqe& e) {
-  const RingDesc R = p.rings[e.sub];
+  const RingDesc& R = p.rings[e.sub];                 // (by reference: the struct holds 64 member pointers)
   const int G = p.G, n = R.nranks, W = p.cacheWays;
   const int c = (int)e.collId;
   CtxSlot* g = &p.ctx[(size_t)c * G + b];
