@@ -49,19 +49,37 @@ def main():
         cq = [[t for t, e, c, x in ev if e == "cqe" and c == cid] for ev in tr]
         k = min(len(f) for f in fetch)
         spread, last_to_sw, sw_to_done, done_to_cqe, first_sw_spread = [], [], [], [], []
+        own_admit_to_sw, others_after_last, mirror_to_admit = [], [], []
+        # every block's "mirror written" marks (mark 4) per rank
+        tr4 = []
+        for r in range(n):
+            ev4 = []
+            for bb in range(G):
+                ev4 += [(t, e, c, x) for t, e, c, x in comms[r].trace(bb) if e == "mark" and x == 4]
+            tr4.append(ev4)
         for j in range(max(0, k - a.reps), k):
             fs = [fetch[r][j] for r in range(n)]
             # first switch-in of this sample on each rank
             sws = [min(t for t in sw[r] if t >= fetch[r][j]) for r in range(n)]
             dns = [min(t for t in dn[r] if t >= sws[r]) for r in range(n)]
             spread.append((max(fs) - min(fs)) / 1e3)
+            last = max(range(n), key=lambda r: fs[r])
+            own_admit_to_sw.append((sws[last] - fs[last]) / 1e3)
+            others_after_last.append(max((sws[r] - fs[last]) / 1e3 for r in range(n) if r != last))
+            # the fetching block's mirror publish (mark 4) of the last rank, before its admission
+            m4 = [t for t, e, c, x in tr4[last] if t <= fs[last]]
+            if m4:
+                mirror_to_admit.append((fs[last] - max(m4)) / 1e3)
             last_to_sw.append((max(sws) - max(fs)) / 1e3)
             first_sw_spread.append((max(sws) - min(sws)) / 1e3)
             sw_to_done.append((max(dns) - max(sws)) / 1e3)
         med = lambda v: round(statistics.median(v), 2)
         out = {"bytes": a.bytes, "e2e_median_us": med(e2e), "samples": len(spread),
                "admission_spread_us": med(spread), "last_admission_to_last_switch_in_us": med(last_to_sw),
-               "switch_in_spread_us": med(first_sw_spread), "last_switch_in_to_last_done_us": med(sw_to_done)}
+               "switch_in_spread_us": med(first_sw_spread), "last_switch_in_to_last_done_us": med(sw_to_done),
+               "last_admitter_admit_to_switch_in_us": med(own_admit_to_sw),
+               "last_admission_to_others_switch_in_us": med(others_after_last),
+               "last_admitter_mirror_to_admit_us": med(mirror_to_admit) if mirror_to_admit else None}
         print(json.dumps(out))
         with open(a.out, "w") as f:
             json.dump(out, f)
