@@ -65,7 +65,8 @@ def test_config_defaults_and_validation():
     for kw in (dict(llSliceBytes=12), dict(llSliceBytes=0), dict(spinNs=0), dict(stagingTiles=7),
                dict(blocksPerSM=3), dict(blocksPerSM=2, blockThreads=608), dict(blockThreads=96),
                dict(blockThreads=640), dict(pipeDepth=9), dict(spinBase=10, spinMin=20), dict(sliceBytes=100),
-               dict(traceCap=1 << 25), dict(l2Hints=4), dict(l2Hints=-1)):
+               dict(traceCap=1 << 25), dict(l2Hints=4), dict(l2Hints=-1), dict(llSpeculate=3),
+               dict(llSpeculate=-1)):
         with pytest.raises(occl.OcclError) as e:
             occl.occlCommCreate(2, 0, 0, occl.occlConfigDefault(**kw))
         assert e.value.code == occl.occlInvalidArgument, kw
@@ -73,6 +74,7 @@ def test_config_defaults_and_validation():
     assert cfg.llMaxBytes > 0 and cfg.llSliceBytes % 8 == 0 and cfg.directMode == 1
     assert cfg.spinNs > 0 and cfg.traceCap == 0 and cfg.blockThreads == 608
     assert cfg.l2Hints == 2                            # evict-first user streams, evict-last connector lines
+    assert cfg.llSpeculate == 2                        # LL runs are the default LL mode
 
 
 def test_product_path_never_touches_oracle():
